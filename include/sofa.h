@@ -1,0 +1,180 @@
+/*
+ * sofa.h — C ABI of the B200-native SOFA exact k-NN path (libsofa.so).
+ *
+ * SOFA = "Fast and Exact Similarity Search in less than a Blink of an Eye" (arxiv 2411.17483),
+ * PAPER.md citations as P:<line>.  The path:
+ *   a1 z-normalisation        Def. 2
+ *   a2 MCB learning           Alg. 1, P:297-325 (variance selection P:248-250)
+ *   a3 SFA transform          Alg. 2, bins P:225-228
+ *   a4 block layout           MESSI tree P:159-166 -> sorted SFA-word blocks + envelopes
+ *   a5 query prep             d_SFA / mind_i tables
+ *   a6 seed + envelope LB     approximate search P:169, leaf LB P:171-173
+ *   a7 word LB scan           Alg. 3, P:398-435 (chunks of 8, early abandon)
+ *   a8 refine + top-k         P:119, ED with early abandoning P:382
+ *   a9 cross-GPU merge        k-NN P:177
+ *
+ * Conventions (every entry point):
+ *  - Array pointers named *_dev are CUDA DEVICE pointers (row-major; float32 / int64 / uint8 /
+ *    float64 as typed).  Pointers named *_host are host pointers.  Struct pointers
+ *    (sofa_model, sofa_build_opts, sofa_knn_stats) are host pointers.
+ *  - `cuda_stream` is a cudaStream_t (may be NULL = legacy default stream).  Work is
+ *    stream-ordered; sofa_build, sofa_learn_model, sofa_get_model and sofa_knn_host return
+ *    after synchronising that stream; sofa_knn, sofa_transform and sofa_merge_topk are
+ *    asynchronous (sofa_knn synchronises only when `stats` is non-NULL).
+ *  - Return value: SOFA_OK (0) or a negative SOFA_E* code; the message of the last failure on
+ *    the calling thread is returned by sofa_last_error().  No C++ exception crosses the ABI.
+ *  - Distances returned are the z-ED d (the square root; reading 13 in DESIGN.md);
+ *    pruning compares squared values internally.  Per query, k results sorted by (d, index)
+ *    ascending, ties to the smaller global index (reading 14); a shard holding fewer than k
+ *    candidates pads with (+inf, -1).
+ *  - Limits: 4 <= len <= 1024, len % 4 == 0; 1 <= l <= min(64, len-1); alphabet a power of two
+ *    in [2, 256]; 1 <= k <= 128; block_size a power of two in [32, 8192].
+ */
+#ifndef SOFA_H_
+#define SOFA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SOFA_OK 0
+#define SOFA_EINVAL (-1)      /* bad argument (message says which) */
+#define SOFA_EDEGENERATE (-2) /* equi-depth sample smaller than the alphabet */
+#define SOFA_ENOMEM (-3)      /* device allocation failed */
+#define SOFA_ECUDA (-4)       /* a CUDA runtime / launch error */
+
+#define SOFA_MAX_L 64
+#define SOFA_MAX_ALPHABET 256
+#define SOFA_MAX_LEN 1024
+#define SOFA_MAX_K 128
+
+#define SOFA_BINNING_EQUI_DEPTH 0 /* BASELINE.json */
+#define SOFA_BINNING_EQUI_WIDTH 1 /* Alg. 1 l.8-11 */
+
+/* Opaque index: owns the SFA words (sorted), per-series (mu, 1/sigma), the permutation,
+ * per-block envelopes, block keys, the model's device tables and query scratch.  It BORROWS
+ * the `series` buffer given to sofa_build (caller keeps it alive and unmodified until
+ * sofa_free): 100M x 256 float32 = 102.4 GB does not fit twice. */
+typedef struct sofa_index sofa_index;
+
+/* Learned MCB model (Alg. 1 returns "bins, best_l").  Plain data so it can be
+ * broadcast as bytes between ranks. */
+typedef struct {
+  int32_t len;       /* series length n */
+  int32_t l;         /* number of selected real values = symbols per word (reading 4) */
+  int32_t alphabet;  /* a */
+  int32_t binning;   /* SOFA_BINNING_* */
+  int32_t best_pos[SOFA_MAX_L];   /* interleaved positions (2k = Re X_k, 2k+1 = Im X_k),
+                                     descending sample variance, ties -> lower position */
+  double weights[SOFA_MAX_L];     /* Eq. 1 weight per selected position: 1 (DC/Nyquist) or 2 */
+  double edges[SOFA_MAX_L * 255]; /* row j: a-1 ascending bin edges beta_j(1..a-1), float64 */
+} sofa_model;
+
+typedef struct {
+  int64_t sample_size;     /* S; 0 => round(sample_ratio * global_n), clamped to [a, global_n] */
+  double sample_ratio;     /* default 0.01 (Alg. 1 r) */
+  int32_t block_size;      /* B series per leaf block, default 256 (reading 19) */
+  int32_t candidate_limit; /* max complex index eligible for selection; 0 => n/2 (reading 3) */
+  int32_t binning;         /* SOFA_BINNING_EQUI_DEPTH (default) or _EQUI_WIDTH */
+  int32_t reserved;
+  int64_t global_offset;   /* global index of this shard's row 0 (0 on one GPU) */
+  int64_t global_n;        /* total rows over all shards (0 => this call's n) */
+  const sofa_model* model; /* nullable: NULL => learn from this call's rows at the global
+                              strided sample indices floor(j*global_n/S) (1 GPU only) */
+} sofa_build_opts;
+
+typedef struct {
+  int64_t queries;
+  int64_t blocks_total;     /* sum over queries of the number of blocks (N/B) */
+  int64_t blocks_survived;  /* blocks whose words were scanned (envelope LB <= threshold) */
+  int64_t words_scanned;    /* SFA words whose LB was evaluated */
+  int64_t candidates;       /* words with LB <= threshold */
+  int64_t refined;          /* exact distance computations started */
+  int64_t abandoned;        /* of those, early-abandoned */
+} sofa_knn_stats;
+
+/* Fill *out with defaults (sample_ratio 0.01, block_size 256, equi-depth, everything else 0). */
+int sofa_default_opts(sofa_build_opts* out);
+
+/* Alg. 1 on an already drawn sample: z-normalise each of the S rows (float64),
+ * full orthonormal DFT at the eligible positions (float64), per-position sample variance
+ * (ddof=1) across the S rows, best_l = the l largest (ties -> lower position), then one row
+ * of a-1 edges per selected position: equi-depth sorted[ceil(i*S/a)] or equi-width
+ * min + i*(max-min)/a.  Deterministic (fixed-order float64 reductions).
+ *   sample_dev: S x len float32, device.  opts: nullable (binning, candidate_limit).
+ *   out: host struct written on success.
+ * Errors: EINVAL (limits), EDEGENERATE (equi-depth and S < alphabet). */
+int sofa_learn_model(const float* sample_dev, int64_t S, int32_t len, int32_t l, int32_t alphabet,
+                     const sofa_build_opts* opts, void* cuda_stream, sofa_model* out);
+
+/* sofa_build(series, n, len, l, alphabet) — BASELINE.json north_star call.
+ * a1 (mu, 1/sigma) + a3 (projection onto the selected positions, quantisation) fused in one
+ * pass over the series, then a4: 64-bit 2-bit-interleaved word keys, radix sort, gather of
+ * sorted words, per-block min/max envelopes.  Learns the model first unless opts->model.
+ *   series_dev: n x len float32 device, BORROWED until sofa_free.  n may be 0 only with
+ *   opts->model (an empty shard).  out: receives the new index.
+ * Errors: EINVAL, EDEGENERATE, ENOMEM, ECUDA. */
+int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32_t alphabet,
+               const sofa_build_opts* opts, void* cuda_stream, sofa_index** out);
+
+/* sofa_knn(queries, q, k) — BASELINE.json north_star call; exact k-NN under z-ED.
+ * One fused persistent kernel: per query a5 tables -> a6 own-key-block seed and envelope LB
+ * scan -> a7 word LB scan (chunks of 8, abandon) -> a8 LB-ordered refine with early
+ * abandoning and top-k.
+ *   queries_dev: q x len float32 device (raw; z-normalised inside).
+ *   bsf_init_dev: nullable, q floats: an upper bound on each query's k-th squared distance
+ *   (e.g. from another shard) used to prune; results above it may be absent (padding).
+ *   out_dist_dev: q x k float32 device; out_idx_dev: q x k int64 device (global indices).
+ *   stats: nullable host struct (if given, the call synchronises and fills it).
+ * Errors: EINVAL (k < 1, k > 128, k > global_n, q < 1), ECUDA. */
+int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, const float* bsf_init_dev,
+             float* out_dist_dev, int64_t* out_idx_dev, sofa_knn_stats* stats, void* cuda_stream);
+
+/* Same as sofa_knn with HOST buffers: copies the queries host->device, runs the search and
+ * copies the results device->host inside the call (end-to-end path).  Synchronous. */
+int sofa_knn_host(sofa_index* ix, const float* queries_host, int32_t q, int32_t k,
+                  float* out_dist_host, int64_t* out_idx_host, sofa_knn_stats* stats, void* cuda_stream);
+
+/* a9: per query, the k smallest (dist, idx) pairs of `parts` lists, each sorted ascending
+ * (padding (+inf,-1) last); ties -> smaller idx.  dist_dev: parts x q x k float32,
+ * idx_dev: parts x q x k int64, outputs q x k.  All device pointers.  Errors: EINVAL, ECUDA. */
+int sofa_merge_topk(const float* dist_dev, const int64_t* idx_dev, int32_t parts, int32_t q, int32_t k,
+                    float* out_dist_dev, int64_t* out_idx_dev, void* cuda_stream);
+
+/* Copy the index's model to *out (host). */
+int sofa_get_model(const sofa_index* ix, sofa_model* out);
+
+/* Parity entry point for a1+a3 (the same kernel sofa_build runs): for n rows, the projected
+ * values (float64, n x l, nullable) and the SFA words (uint8, n x l, nullable) under `model`.
+ * All array pointers device.  Errors: EINVAL, ECUDA. */
+int sofa_transform(const float* series_dev, int64_t n, const sofa_model* model, double* out_values_dev,
+                   uint8_t* out_words_dev, void* cuda_stream);
+
+/* Index introspection for tests: number of rows / blocks / block size / word stride. */
+typedef struct {
+  int64_t n, n_blocks, global_offset, global_n;
+  int32_t len, l, alphabet, block_size, word_stride;
+} sofa_index_info;
+int sofa_get_info(const sofa_index* ix, sofa_index_info* out);
+
+/* Copy the index arrays into caller device buffers (any may be NULL):
+ * words_sorted n x word_stride uint8, perm n int32 (sorted position -> local row),
+ * envelopes n_blocks x 2 x word_stride uint8 (min row then max row), block_keys n_blocks uint64. */
+int sofa_export_index(const sofa_index* ix, uint8_t* words_sorted_dev, int32_t* perm_dev, uint8_t* env_dev,
+                      uint64_t* block_keys_dev, void* cuda_stream);
+
+/* Release everything the index owns (never the borrowed series). NULL is a no-op. */
+void sofa_free(sofa_index* ix);
+
+/* Thread-local message of the last failure ("" if none). */
+const char* sofa_last_error(void);
+
+/* Process-wide count of kernels this library has launched (bench evidence). */
+int64_t sofa_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOFA_H_ */

@@ -1,0 +1,175 @@
+// Shared device helpers and the internal index layout of libsofa (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/sofa.h"
+
+namespace sofa {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kThreads = 256;  // every kernel of the hot path runs 8 warps per CTA
+
+extern std::atomic<int64_t> g_launches;
+void set_error(const std::string& msg);
+
+#define SOFA_CK(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      ::sofa::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));           \
+      return e_ == cudaErrorMemoryAllocation ? SOFA_ENOMEM : SOFA_ECUDA;               \
+    }                                                                                  \
+  } while (0)
+
+#define SOFA_LAUNCHED()                                                                \
+  do {                                                                                 \
+    ::sofa::g_launches.fetch_add(1);                                                   \
+    cudaError_t e_ = cudaGetLastError();                                               \
+    if (e_ != cudaSuccess) {                                                           \
+      ::sofa::set_error(std::string("kernel launch: ") + cudaGetErrorString(e_));      \
+      return SOFA_ECUDA;                                                               \
+    }                                                                                  \
+  } while (0)
+
+// Device-side copy of the model: LT = l rounded up to 16/32/64 (padded rows are inert:
+// zero basis, +inf edges, zero tables).
+struct DevModel {
+  int len, l, LT, a, a_bits, WS;  // WS = word stride in bytes (l rounded up to 16)
+  const float* basis32;            // LT x len   float32 cos/-sin(2 pi k t/n)/sqrt(n)
+  const double* basis64;           // LT x len   float64 (query projection)
+  const float* edges32;            // LT x 256   float32, row padded with +inf
+  const double* edges64;           // LT x 256   float64, row padded with +inf
+  float weights[SOFA_MAX_L];
+};
+
+// ---------------------------------------------------------------------------------------------
+// streaming loads (read-once data: do not allocate in L1)
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(FULL, v, m);
+  return v;
+}
+__device__ __forceinline__ float warp_sum_f32(float v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(FULL, v, m);
+  return v;
+}
+
+// a1 (Def. 2, population std, reading 1): per-row statistics computed by ONE warp with
+// a fixed arithmetic order, shared by the series transform and the query prep so that a query
+// equal to a stored row z-normalises to the same float32 bits (exact duplicates -> d = 0).
+// Each lane sums its float4s (lane + 32 f) in float32, the 32 partials are combined in float64.
+// Returns mu (float32), inv_sigma (float64; 0 for a constant row), and the float64 mu.
+template <int NF>
+__device__ __forceinline__ void row_stats(const float4 (&x)[NF], int nf4, int len, float& muf, double& mu64,
+                                          double& inv64) {
+  const int lane = threadIdx.x & 31;
+  float p = 0.f;
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+    if (lane + 32 * f < nf4) p = __fadd_rn(p, __fadd_rn(__fadd_rn(x[f].x, x[f].y), __fadd_rn(x[f].z, x[f].w)));
+  mu64 = warp_sum_f64((double)p) / (double)len;
+  muf = (float)mu64;
+  float s = 0.f;
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+    if (lane + 32 * f < nf4) {
+      float a = __fsub_rn(x[f].x, muf), b = __fsub_rn(x[f].y, muf);
+      float c = __fsub_rn(x[f].z, muf), d = __fsub_rn(x[f].w, muf);
+      s = __fadd_rn(s, __fadd_rn(__fmaf_rn(a, a, __fmul_rn(b, b)), __fmaf_rn(c, c, __fmul_rn(d, d))));
+    }
+  double var = warp_sum_f64((double)s) / (double)len;
+  double sd = sqrt(var);
+  inv64 = sd < 1e-12 ? 0.0 : 1.0 / sd;
+}
+
+// upper_bound over a 256-entry edge row padded with +inf: number of edges <= v (symbol of v;
+// bins [beta(s), beta(s+1)) — P:225-228, value on an edge goes right).
+template <typename E>
+__device__ __forceinline__ int bin_of(const E* __restrict__ e, double v) {
+  int pos = 0;
+#pragma unroll
+  for (int step = 128; step >= 1; step >>= 1)
+    if ((double)e[pos + step - 1] <= v) pos += step;
+  return pos;
+}
+
+// 64-bit block-ordering key of a word (a4): symbols normalised to 8 bits, 2-bit groups taken
+// MSB-first round-robin over the first min(l,16) positions (SURVEY SIM-4: 2-bit interleaving
+// gives the fewest surviving blocks).  Only the order of blocks depends on it, never a result.
+__device__ __forceinline__ uint64_t word_key(const uint8_t* w, int l, int a_bits) {
+  const int P = l < 16 ? l : 16;
+  uint64_t key = 0;
+  int nbits = 0;
+  for (int r = 0; r < 4 && nbits < 64; ++r)
+    for (int p = 0; p < P && nbits < 64; ++p) {
+      uint32_t s8 = ((uint32_t)w[p] << (8 - a_bits)) & 0xffu;
+      key = (key << 2) | ((s8 >> (6 - 2 * r)) & 3u);
+      nbits += 2;
+    }
+  return nbits < 64 ? key << (64 - nbits) : key;
+}
+
+}  // namespace sofa
+
+// Host-side index object (opaque in the C ABI).
+struct sofa_index {
+  int64_t n = 0, nb = 0, global_offset = 0, global_n = 0;
+  int32_t len = 0, l = 0, a = 0, B = 256, LT = 16, WS = 16;
+  sofa_model model{};
+  const float* series = nullptr;  // borrowed
+  uint8_t* words = nullptr;       // n x WS, sorted by key
+  float2* stats = nullptr;        // n, sorted order: (mu, 1/sigma)
+  int32_t* perm = nullptr;        // n: sorted position -> local row
+  uint8_t* env = nullptr;         // nb x 2 x WS
+  uint64_t* bkey = nullptr;       // nb first keys
+  float* basis32 = nullptr;
+  double* basis64 = nullptr;
+  float* edges32 = nullptr;
+  double* edges64 = nullptr;
+  // query scratch
+  unsigned long long* gscratch = nullptr;
+  int64_t gscratch_ctas = 0;
+  int* qcounter = nullptr;
+  unsigned long long* dstats = nullptr;
+  // host-path staging
+  float* hq_dev = nullptr;
+  float* hd_dev = nullptr;
+  int64_t* hi_dev = nullptr;
+  int64_t h_cap = 0;
+  int device = 0;
+  sofa::DevModel dm{};
+};
+
+namespace sofa {
+int upload_model(const sofa_model& m, int len, sofa_index* ix, cudaStream_t st);
+int launch_transform(const float* X, int64_t N, const DevModel& dm, uint8_t* words, float2* stats, uint64_t* keys,
+                     double* vals, uint8_t* words_l, cudaStream_t st);
+int launch_envelopes(const uint8_t* words, int64_t n, int B, int WS, const uint64_t* skeys, uint8_t* env,
+                     uint64_t* bkey, cudaStream_t st);
+int launch_gather(const uint8_t* words, const float2* stats, const int32_t* perm, int64_t n, int WS,
+                  uint8_t* words_out, float2* stats_out, cudaStream_t st);
+int learn_model_dev(const float* sample, int64_t S, int len, int l, int a, int binning, int cand_limit,
+                    cudaStream_t st, sofa_model* out);
+int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
+                 cudaStream_t st);
+int launch_merge(const float* d, const int64_t* i, int parts, int q, int k, float* od, int64_t* oi, cudaStream_t st);
+int launch_fill_pad(float* od, int64_t* oi, int64_t cnt, cudaStream_t st);
+}  // namespace sofa

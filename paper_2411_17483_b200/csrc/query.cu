@@ -1,0 +1,563 @@
+// a5..a8: the exact k-NN query path as ONE persistent kernel (one CTA of 8 warps per query at a
+// time; CTAs pull queries from an atomic counter so uneven per-query work balances out).
+//
+// Per query:
+//   a5  z-norm (shared row_stats, float32 q-hat for the refine, float64 for the projection),
+//       float64 projection onto the l selected positions, then three l x 256 tables in shared
+//       memory, each entry rounded DOWN to float32 (reading 15):
+//         T  [j][s] = w_j * mind_j(q_j, s)^2                   word LB  (d_SFA)
+//         Tlo[j][s] = w_j * max(0, beta_j(s)   - q_j)^2        envelope lower side
+//         Thi[j][s] = w_j * max(0, q_j - beta_j(s+1))^2        envelope upper side
+//   a6  seed: the query's own-key block (MESSI's approximate search) found by a
+//       256-way parallel search over the blocks' first keys, scanned + refined -> BSF0;
+//       then the envelope LB of every block (leaf LB); blocks with LB <= thr are
+//       appended to a per-CTA list and, when <= CAP_B of them survive, bitonic-sorted by LB in
+//       shared memory (MESSI's priority queue: process leaves in ascending LB, stop
+//       at the first whose LB exceeds the BSF).
+//   a7  word LB scan of the listed blocks in batches of CAP_C words: 16-byte word loads, table
+//       gathers in chunks of 8 positions with early abandoning (Alg. 3), survivors
+//       appended to a shared candidate buffer (warp-aggregated atomics).
+//   a8  candidates sorted by LB, refined in waves of 8 (one warp per candidate, float4 row
+//       loads, warp-shuffle reduction, early abandoning per 256-element chunk vs BSF),
+//       top-k kept sorted by (d^2, index); refinement stops at the first candidate whose LB
+//       exceeds the threshold.
+// thr = BSF * (1 + 1e-4) + 1e-5 (squared units): prune only when the float32 lower bound clearly
+// exceeds the float32 k-th best; this absorbs the data-side projection error (reading 15).
+#include "common.cuh"
+
+namespace sofa {
+
+constexpr int CAP_B = 2048;  // surviving blocks sorted in shared memory
+constexpr int CAP_C = 1024;  // words per scan batch = candidate buffer capacity
+constexpr int KMAX = SOFA_MAX_K;
+
+struct QArgs {
+  const float* series;
+  int64_t n, nb;
+  int len, l, a, WS, B;
+  const uint8_t* words;
+  const float2* stats;
+  const int32_t* perm;
+  const uint8_t* env;
+  const uint64_t* bkey;
+  const double* edges64;
+  const double* basis64;
+  const float* Q;
+  int q, k;
+  const float* bsf_init;
+  float* od;
+  int64_t* oi;
+  int64_t goff;
+  unsigned long long* gscratch;
+  int* qcounter;
+  unsigned long long* dstats;
+  float weights[SOFA_MAX_L];
+};
+
+__device__ __forceinline__ float thr_of(float bsf) { return isinf(bsf) ? INFINITY : bsf * (1.0f + 1e-4f) + 1e-5f; }
+
+__device__ __forceinline__ unsigned long long pack(float lb, uint32_t id) {
+  return ((unsigned long long)__float_as_uint(lb) << 32) | id;
+}
+__device__ __forceinline__ float lb_of(unsigned long long e) { return __uint_as_float((uint32_t)(e >> 32)); }
+
+__device__ void bitonic_sort_u64(unsigned long long* s, int n) {
+  int P2 = 1;
+  while (P2 < n) P2 <<= 1;
+  for (int i = n + threadIdx.x; i < P2; i += kThreads) s[i] = ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= P2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P2; i += kThreads) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long a = s[i], b = s[ixj];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            s[i] = b;
+            s[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// warp-aggregated append of (key) into buf[*counter ...]
+__device__ __forceinline__ void warp_append(bool pass, unsigned long long key, unsigned long long* buf, int* counter) {
+  const unsigned m = __ballot_sync(FULL, pass);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(counter, __popc(m));
+  base = __shfl_sync(FULL, base, leader);
+  if (pass) buf[base + __popc(m & ((1u << lane) - 1u))] = key;
+}
+
+struct QShared {
+  int qi, cnt, ncand, tkn, b0;
+  float bsf, bsf_init, thr;
+  unsigned long long st[6];  // blocks_survived, words_scanned, candidates, refined, abandoned, -
+};
+
+// exact squared z-ED with early abandoning (a8): one warp, float4 loads, chunk = 2 float4 / lane
+template <int NF>
+__device__ __forceinline__ float ed_warp(const float* __restrict__ row, float2 st, const float4* s_qh4, int nf4,
+                                         float bsf, bool& abandoned) {
+  const int lane = threadIdx.x & 31;
+  const float4* r4 = reinterpret_cast<const float4*>(row);
+  float total = 0.f;
+  abandoned = false;
+  constexpr int CH = NF < 2 ? NF : 2;
+#pragma unroll
+  for (int f0 = 0; f0 < NF; f0 += CH) {
+    float4 x[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int fi = lane + 32 * (f0 + c);
+      x[c] = fi < nf4 ? ld_stream(r4 + fi) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int fi = lane + 32 * (f0 + c);
+      if (fi < nf4) {
+        const float4 q = s_qh4[fi];
+        const float d0 = __fsub_rn(__fmul_rn(__fsub_rn(x[c].x, st.x), st.y), q.x);
+        const float d1 = __fsub_rn(__fmul_rn(__fsub_rn(x[c].y, st.x), st.y), q.y);
+        const float d2 = __fsub_rn(__fmul_rn(__fsub_rn(x[c].z, st.x), st.y), q.z);
+        const float d3 = __fsub_rn(__fmul_rn(__fsub_rn(x[c].w, st.x), st.y), q.w);
+        acc = __fmaf_rn(d0, d0, acc);
+        acc = __fmaf_rn(d1, d1, acc);
+        acc = __fmaf_rn(d2, d2, acc);
+        acc = __fmaf_rn(d3, d3, acc);
+      }
+    }
+    total += warp_sum_f32(acc);
+    if (f0 + CH < NF && total > bsf) {
+      abandoned = true;
+      return total;
+    }
+  }
+  return total;
+}
+
+// word LB (d_SFA^2 from the T table) with chunked early abandoning: Alg. 3
+template <int LT>
+__device__ __forceinline__ float word_lb(const uint8_t* __restrict__ wp, const float* __restrict__ sT, float thr) {
+  float lb = 0.f;
+#pragma unroll
+  for (int c = 0; c < LT / 16; ++c) {
+    const uint4 w = ld_stream_u4(wp + 16 * c);
+    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // two chunks of 8 positions per 16 bytes
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = c * 16 + h * 8 + jj;
+        const uint32_t sym = (wv[(h * 8 + jj) >> 2] >> (8 * (jj & 3))) & 0xffu;
+        lb += sT[j * 256 + sym];
+      }
+      if (lb > thr) return lb;
+    }
+  }
+  return lb;
+}
+
+template <int LT, int NF>
+__device__ void refine_candidates(const QArgs& A, QShared& S, unsigned long long* s_cand, float* s_tkd, int* s_tki,
+                                  float* s_wd, int* s_wi, const float4* s_qh4) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nc = S.ncand;
+  if (nc == 0) return;
+  if (nc > 8) bitonic_sort_u64(s_cand, nc);
+  const int nf4 = A.len >> 2;
+  for (int base = 0; base < nc; base += 8) {
+    const float thr = S.thr, bsf = S.bsf;
+    const int c = base + warp;
+    float d2 = INFINITY;
+    int oidx = -1;
+    bool did = false, ab = false;
+    if (c < nc) {
+      const unsigned long long e = s_cand[c];
+      if (lb_of(e) <= thr) {
+        did = true;
+        const uint32_t pos = (uint32_t)e;
+        oidx = A.perm[pos];
+        const float2 st = A.stats[pos];
+        d2 = ed_warp<NF>(A.series + (int64_t)oidx * A.len, st, s_qh4, nf4, bsf, ab);
+      }
+    }
+    if (lane == 0) {
+      s_wd[warp] = (did && !ab) ? d2 : INFINITY;
+      s_wi[warp] = (did && !ab) ? oidx : -1;
+      if (did) atomicAdd(&S.st[3], 1ull);
+      if (ab) atomicAdd(&S.st[4], 1ull);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const int k = A.k;
+      for (int w = 0; w < 8; ++w) {
+        const int i = s_wi[w];
+        if (i < 0) continue;
+        const float d = s_wd[w];
+        const int n = S.tkn;
+        if (n < k || d < s_tkd[n - 1] || (d == s_tkd[n - 1] && i < s_tki[n - 1])) {
+          int p = n < k ? n : k - 1;
+          while (p > 0 && (s_tkd[p - 1] > d || (s_tkd[p - 1] == d && s_tki[p - 1] > i))) {
+            s_tkd[p] = s_tkd[p - 1];
+            s_tki[p] = s_tki[p - 1];
+            --p;
+          }
+          s_tkd[p] = d;
+          s_tki[p] = i;
+          if (n < k) S.tkn = n + 1;
+        }
+      }
+      if (S.tkn == k) S.bsf = fminf(S.bsf_init, s_tkd[k - 1]);
+      S.thr = thr_of(S.bsf);
+    }
+    __syncthreads();
+    if (base + 8 < nc && lb_of(s_cand[base + 8]) > S.thr) break;
+  }
+  __syncthreads();
+  if (tid == 0) S.ncand = 0;
+  __syncthreads();
+}
+
+// scan the words of the listed blocks (a7) and refine (a8), batch by batch
+template <int LT, int NF>
+__device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long* list, int cnt, bool sorted,
+                            const float* s_T, unsigned long long* s_cand, float* s_tkd, int* s_tki, float* s_wd,
+                            int* s_wi, const float4* s_qh4) {
+  const int tid = threadIdx.x;
+  const int B = A.B;
+  const int G = B <= CAP_C ? CAP_C / B : 1;    // blocks per batch
+  const int SUB = B <= CAP_C ? 1 : B / CAP_C;  // batches per block
+  const int span = B <= CAP_C ? B : CAP_C;
+  for (int e0 = 0; e0 < cnt; e0 += G) {
+    for (int sub = 0; sub < SUB; ++sub) {
+      const float thr = S.thr;
+      if (sorted && lb_of(list[e0]) > thr) return;  // every later block has a larger LB
+      if (tid == 0 && sub == 0) {
+        unsigned long long surv = 0;
+        for (int u = 0; u < G && e0 + u < cnt; ++u) surv += lb_of(list[e0 + u]) <= thr;
+        S.st[0] += surv;
+      }
+      unsigned long long scanned = 0;
+      for (int w = tid; w < CAP_C; w += kThreads) {
+        const int u = w / span, m = w % span;
+        const int e = e0 + u;
+        bool valid = e < cnt && u < G;
+        int64_t pos = 0;
+        if (valid) {
+          const unsigned long long ent = list[e];
+          pos = (int64_t)(uint32_t)ent * B + (int64_t)sub * CAP_C + m;
+          valid = lb_of(ent) <= thr && pos < A.n;
+        }
+        float lb = INFINITY;
+        if (valid) lb = word_lb<LT>(A.words + pos * A.WS, s_T, thr);
+        scanned += valid;
+        warp_append(valid && lb <= thr, pack(lb, (uint32_t)pos), s_cand, &S.ncand);
+      }
+      if (scanned) atomicAdd(&S.st[1], scanned);
+      __syncthreads();
+      if (tid == 0) S.st[2] += S.ncand;
+      refine_candidates<LT, NF>(A, S, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+    }
+  }
+}
+
+template <int LT, int NF>
+__global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ QShared S;
+  constexpr int UB0 = 2 * LT * 256 * 4, UB1 = CAP_B * 8, UB2 = NF * 128 * 8;
+  constexpr int UB = UB0 > UB1 ? (UB0 > UB2 ? UB0 : UB2) : (UB1 > UB2 ? UB1 : UB2);
+  float4* s_qh4 = reinterpret_cast<float4*>(smem);                         // NF*32 float4
+  double* s_qproj = reinterpret_cast<double*>(smem + NF * 128 * 4);        // LT
+  float* s_T = reinterpret_cast<float*>(smem + NF * 128 * 4 + LT * 8);     // LT*256
+  unsigned char* s_u = smem + NF * 128 * 4 + LT * 8 + LT * 256 * 4;        // union
+  float* s_Tlo = reinterpret_cast<float*>(s_u);
+  float* s_Thi = s_Tlo + LT * 256;
+  double* s_qd = reinterpret_cast<double*>(s_u);
+  unsigned long long* s_blist = reinterpret_cast<unsigned long long*>(s_u);
+  unsigned long long* s_cand = reinterpret_cast<unsigned long long*>(s_u + UB);
+  float* s_tkd = reinterpret_cast<float*>(s_cand + CAP_C);
+  int* s_tki = reinterpret_cast<int*>(s_tkd + KMAX);
+  float* s_wd = reinterpret_cast<float*>(s_tki + KMAX);
+  int* s_wi = reinterpret_cast<int*>(s_wd + 8);
+  __shared__ uint8_t s_qw[SOFA_MAX_L];
+  __shared__ unsigned long long s_seed;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int len = A.len, nf4 = len >> 2, l = A.l, a = A.a;
+  unsigned long long* gl = A.gscratch + (int64_t)blockIdx.x * A.nb;
+
+  for (;;) {
+    if (tid == 0) S.qi = atomicAdd(A.qcounter, 1);
+    __syncthreads();
+    const int qi = S.qi;
+    if (qi >= A.q) break;
+    // ---------------------------------------------------------------- a5: z-norm + projection
+    if (warp == 0) {
+      const float4* q4 = reinterpret_cast<const float4*>(A.Q + (int64_t)qi * len);
+      float4 x[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        const int fi = lane + 32 * f;
+        x[f] = fi < nf4 ? q4[fi] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float muf;
+      double mu64, inv64;
+      row_stats<NF>(x, nf4, len, muf, mu64, inv64);
+      const float invf = (float)inv64;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        const int fi = lane + 32 * f;
+        if (fi < nf4) {
+          float4 h;
+          h.x = __fmul_rn(__fsub_rn(x[f].x, muf), invf);
+          h.y = __fmul_rn(__fsub_rn(x[f].y, muf), invf);
+          h.z = __fmul_rn(__fsub_rn(x[f].z, muf), invf);
+          h.w = __fmul_rn(__fsub_rn(x[f].w, muf), invf);
+          s_qh4[fi] = h;
+          s_qd[4 * fi + 0] = ((double)x[f].x - mu64) * inv64;
+          s_qd[4 * fi + 1] = ((double)x[f].y - mu64) * inv64;
+          s_qd[4 * fi + 2] = ((double)x[f].z - mu64) * inv64;
+          s_qd[4 * fi + 3] = ((double)x[f].w - mu64) * inv64;
+        }
+      }
+      if (lane == 0) {
+        S.cnt = 0;
+        S.ncand = 0;
+        S.tkn = 0;
+        for (int i = 0; i < 6; ++i) S.st[i] = 0;
+        const float bi = A.bsf_init ? A.bsf_init[qi] : INFINITY;
+        S.bsf_init = bi;
+        S.bsf = bi;
+        S.thr = thr_of(bi);
+      }
+    }
+    __syncthreads();
+    for (int j = warp; j < LT; j += 8) {
+      double acc = 0.0;
+      if (j < l)
+        for (int t = lane; t < len; t += 32) acc = fma(s_qd[t], A.basis64[(int64_t)j * len + t], acc);
+      acc = warp_sum_f64(acc);
+      if (lane == 0) s_qproj[j] = acc;
+    }
+    __syncthreads();
+    // ---------------------------------------------------------------- a5: LB tables (round down)
+    for (int e = tid; e < LT * 256; e += kThreads) {
+      const int j = e >> 8, s = e & 255;
+      float t = 0.f, tlo = 0.f, thi = 0.f;
+      if (j < l && s < a) {
+        const double qv = s_qproj[j], w = (double)A.weights[j];
+        const double lo = s == 0 ? -INFINITY : A.edges64[j * 256 + s - 1];
+        const double hi = s == a - 1 ? INFINITY : A.edges64[j * 256 + s];
+        const double dl = fmax(0.0, lo - qv), dh = fmax(0.0, qv - hi);
+        tlo = __double2float_rd(w * dl * dl);
+        thi = __double2float_rd(w * dh * dh);
+        t = __double2float_rd(w * (dl * dl + dh * dh));
+        if (lo <= qv && qv < hi) s_qw[j] = (uint8_t)s;  // the query's own symbol
+      }
+      if (j >= l && s == 0 && j < SOFA_MAX_L) s_qw[j] = 0;
+      s_T[e] = t;
+      s_Tlo[e] = tlo;
+      s_Thi[e] = thi;
+    }
+    __syncthreads();
+    // ---------------------------------------------------------------- a6: seed block
+    const uint64_t key = word_key(s_qw, l, 31 - __clz(a));
+    int64_t lo = 0, hi = A.nb;
+    while (hi - lo > 1) {  // 256-way parallel search: largest b with bkey[b] <= key
+      const int64_t step = (hi - lo + kThreads - 1) / kThreads;
+      const int64_t idx = lo + (int64_t)tid * step;
+      const int c = __syncthreads_count(idx < hi && A.bkey[idx] <= key);
+      if (c == 0) {
+        hi = lo + 1;
+        break;
+      }
+      const int64_t nlo = lo + (int64_t)(c - 1) * step;
+      hi = nlo + step < hi ? nlo + step : hi;
+      lo = nlo;
+    }
+    const int64_t b0 = lo;
+    if (tid == 0) s_seed = pack(0.f, (uint32_t)b0);
+    __syncthreads();
+    scan_blocks<LT, NF>(A, S, &s_seed, A.nb > 0 ? 1 : 0, true, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+    // ---------------------------------------------------------------- a6: envelope LB scan
+    {
+      const float thr = S.thr;
+      const int WS = A.WS;
+      for (int64_t bb = (int64_t)warp * 32; bb < A.nb; bb += kThreads) {
+        const int64_t b = bb + lane;
+        const bool valid = b < A.nb && b != b0;
+        float lb = INFINITY;
+        if (valid) {
+          const uint8_t* ev = A.env + b * 2 * WS;
+          lb = 0.f;
+#pragma unroll
+          for (int c = 0; c < LT / 16; ++c) {
+            const uint4 mn = ld_stream_u4(ev + 16 * c), mx = ld_stream_u4(ev + WS + 16 * c);
+            const uint32_t vn[4] = {mn.x, mn.y, mn.z, mn.w}, vx[4] = {mx.x, mx.y, mx.z, mx.w};
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const int j = c * 16 + jj;
+              lb += s_Tlo[j * 256 + ((vn[jj >> 2] >> (8 * (jj & 3))) & 0xffu)];
+              lb += s_Thi[j * 256 + ((vx[jj >> 2] >> (8 * (jj & 3))) & 0xffu)];
+            }
+          }
+        }
+        warp_append(valid && lb <= thr, pack(lb, (uint32_t)b), gl, &S.cnt);
+      }
+    }
+    __syncthreads();
+    const int cnt = S.cnt;
+    const unsigned long long* list = gl;
+    bool sorted = false;
+    if (cnt <= CAP_B) {  // Tlo/Thi are dead now: the union holds the block list
+      for (int i = tid; i < cnt; i += kThreads) s_blist[i] = gl[i];
+      __syncthreads();
+      bitonic_sort_u64(s_blist, cnt);
+      list = s_blist;
+      sorted = true;
+    }
+    // ---------------------------------------------------------------- a7 + a8
+    scan_blocks<LT, NF>(A, S, list, cnt, sorted, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+    // ---------------------------------------------------------------- output
+    for (int r = tid; r < A.k; r += kThreads) {
+      const bool ok = r < S.tkn;
+      A.od[(int64_t)qi * A.k + r] = ok ? sqrtf(s_tkd[r]) : INFINITY;
+      A.oi[(int64_t)qi * A.k + r] = ok ? A.goff + s_tki[r] : -1;
+    }
+    if (tid == 0 && A.dstats) {
+      atomicAdd(&A.dstats[0], 1ull);
+      atomicAdd(&A.dstats[1], (unsigned long long)A.nb);
+      for (int i = 0; i < 5; ++i) atomicAdd(&A.dstats[2 + i], S.st[i]);
+    }
+    __syncthreads();
+  }
+}
+
+template <int LT, int NF>
+static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
+  QArgs A = A0;
+  constexpr int UB0 = 2 * LT * 256 * 4, UB1 = CAP_B * 8, UB2 = NF * 128 * 8;
+  constexpr int UB = UB0 > UB1 ? (UB0 > UB2 ? UB0 : UB2) : (UB1 > UB2 ? UB1 : UB2);
+  const size_t smem = NF * 128 * 4 + LT * 8 + LT * 256 * 4 + UB + CAP_C * 8 + KMAX * 8 + 8 * 8;
+  auto kern = k_query<LT, NF>;
+  SOFA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0, sms = 148;
+  SOFA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+  if (per_sm < 1) per_sm = 1;
+  int grid = sms * per_sm;
+  if (grid > A.q) grid = A.q;
+  const int64_t need = (int64_t)grid * (ix->nb > 0 ? ix->nb : 1);
+  if (ix->gscratch_ctas < need) {
+    if (ix->gscratch) cudaFree(ix->gscratch);
+    ix->gscratch = nullptr;
+    SOFA_CK(cudaMalloc(&ix->gscratch, need * 8));
+    ix->gscratch_ctas = need;
+  }
+  A.gscratch = ix->gscratch;
+  SOFA_CK(cudaMemsetAsync(ix->qcounter, 0, sizeof(int), st));
+  kern<<<grid, kThreads, smem, st>>>(A);
+  SOFA_LAUNCHED();
+  return SOFA_OK;
+}
+
+int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
+                 cudaStream_t st) {
+  QArgs A{};
+  A.series = ix->series;
+  A.n = ix->n;
+  A.nb = ix->nb;
+  A.len = ix->len;
+  A.l = ix->l;
+  A.a = ix->a;
+  A.WS = ix->WS;
+  A.B = ix->B;
+  A.words = ix->words;
+  A.stats = ix->stats;
+  A.perm = ix->perm;
+  A.env = ix->env;
+  A.bkey = ix->bkey;
+  A.edges64 = ix->edges64;
+  A.basis64 = ix->basis64;
+  A.Q = Q;
+  A.q = q;
+  A.k = k;
+  A.bsf_init = bsf_init;
+  A.od = od;
+  A.oi = oi;
+  A.goff = ix->global_offset;
+  A.qcounter = ix->qcounter;
+  A.dstats = ix->dstats;
+  for (int j = 0; j < SOFA_MAX_L; ++j) A.weights[j] = j < ix->l ? (float)ix->model.weights[j] : 0.f;
+  const int nf4 = ix->len / 4;
+  const int NF = nf4 <= 32 ? 1 : nf4 <= 64 ? 2 : nf4 <= 128 ? 4 : 8;
+#define SOFA_Q(lt, nf) \
+  if (ix->LT == lt && NF == nf) return launch_query_t<lt, nf>(ix, A, st);
+  SOFA_Q(16, 1) SOFA_Q(16, 2) SOFA_Q(16, 4) SOFA_Q(16, 8)
+  SOFA_Q(32, 1) SOFA_Q(32, 2) SOFA_Q(32, 4) SOFA_Q(32, 8)
+  SOFA_Q(64, 1) SOFA_Q(64, 2) SOFA_Q(64, 4) SOFA_Q(64, 8)
+#undef SOFA_Q
+  set_error("query: unsupported (len, l)");
+  return SOFA_EINVAL;
+}
+
+// ---------------------------------------------------------------------------------------------
+// a9: min-merge of `parts` sorted (dist, idx) lists per query; ties -> smaller index.
+__global__ void k_merge_topk(const float* __restrict__ d, const int64_t* __restrict__ ix, int parts, int q, int k,
+                             float* __restrict__ od, int64_t* __restrict__ oi) {
+  const int qi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (qi >= q) return;
+  int head[64];
+  for (int p = 0; p < parts; ++p) head[p] = 0;
+  for (int r = 0; r < k; ++r) {
+    int best = -1;
+    float bd = INFINITY;
+    int64_t bi = -1;
+    for (int p = 0; p < parts; ++p) {
+      if (head[p] >= k) continue;
+      const int64_t o = ((int64_t)p * q + qi) * k + head[p];
+      const int64_t ci = ix[o];
+      if (ci < 0) continue;
+      const float cd = d[o];
+      if (best < 0 || cd < bd || (cd == bd && ci < bi)) {
+        best = p;
+        bd = cd;
+        bi = ci;
+      }
+    }
+    if (best >= 0) head[best]++;
+    od[(int64_t)qi * k + r] = best >= 0 ? bd : INFINITY;
+    oi[(int64_t)qi * k + r] = best >= 0 ? bi : -1;
+  }
+}
+
+int launch_merge(const float* d, const int64_t* i, int parts, int q, int k, float* od, int64_t* oi, cudaStream_t st) {
+  k_merge_topk<<<(q + 127) / 128, 128, 0, st>>>(d, i, parts, q, k, od, oi);
+  SOFA_LAUNCHED();
+  return SOFA_OK;
+}
+
+__global__ void k_fill_pad(float* od, int64_t* oi, int64_t cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+    od[i] = INFINITY;
+    oi[i] = -1;
+  }
+}
+
+int launch_fill_pad(float* od, int64_t* oi, int64_t cnt, cudaStream_t st) {
+  if (cnt <= 0) return SOFA_OK;
+  k_fill_pad<<<(int)((cnt + 255) / 256 < 1024 ? (cnt + 255) / 256 : 1024), 256, 0, st>>>(od, oi, cnt);
+  SOFA_LAUNCHED();
+  return SOFA_OK;
+}
+
+}  // namespace sofa

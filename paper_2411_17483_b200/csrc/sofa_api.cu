@@ -1,0 +1,408 @@
+// C ABI of libsofa (include/sofa.h): argument checks, index construction (a1-a4), query entry
+// points (a5-a8), merge (a9).  Host orchestration only — every step of the path runs in the
+// kernels of transform.cu / learn.cu / query.cu.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sofa {
+
+std::atomic<int64_t> g_launches{0};
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+static bool pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+static int check_shape(int64_t len, int64_t l, int64_t a) {
+  if (len < 4 || len > SOFA_MAX_LEN || len % 4 != 0)
+    return fail(SOFA_EINVAL, "len must be a multiple of 4 in [4, 1024]");
+  if (l < 1 || l > SOFA_MAX_L || l > len - 1) return fail(SOFA_EINVAL, "l must be in [1, min(64, len-1)]");
+  if (a < 2 || a > SOFA_MAX_ALPHABET || !pow2(a)) return fail(SOFA_EINVAL, "alphabet must be a power of two in [2, 256]");
+  return SOFA_OK;
+}
+
+// basis rows for the selected positions: [LT][len], rows >= l are zero
+__global__ void k_basis_sel(const int* __restrict__ pos, int l, int LT, int len, double* __restrict__ b64,
+                            float* __restrict__ b32) {
+  const double rs = 1.0 / sqrt((double)len);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < LT * len; i += gridDim.x * blockDim.x) {
+    const int j = i / len, t = i % len;
+    double v = 0.0;
+    if (j < l) {
+      const int k = pos[j] >> 1, im = pos[j] & 1;
+      const int m = (int)(((int64_t)k * t) % len);
+      double sn, cs;
+      sincospi(2.0 * m / len, &sn, &cs);
+      v = im ? -sn * rs : cs * rs;
+    }
+    b64[i] = v;
+    b32[i] = (float)v;
+  }
+}
+
+__global__ void k_iota(int32_t* p, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (int32_t)i;
+}
+
+// Alg. 1 l.2 sample(X, r): rows floor(j * global_n / S) - offset (reading 6)
+__global__ void k_gather_sample(const float* __restrict__ X, int64_t S, int64_t gn, int64_t off, int len,
+                                float* __restrict__ out) {
+  const int64_t tot = S * len;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i / len, t = i % len;
+    const int64_t row = (j * gn) / S - off;
+    out[i] = X[row * len + t];
+  }
+}
+
+int upload_model(const sofa_model& m, int len, sofa_index* ix, cudaStream_t st) {
+  const int l = m.l, a = m.alphabet;
+  const int LT = l <= 16 ? 16 : l <= 32 ? 32 : 64;
+  ix->LT = LT;
+  ix->WS = (l + 15) / 16 * 16;
+  std::vector<double> e64((size_t)LT * 256, INFINITY);
+  std::vector<float> e32((size_t)LT * 256, INFINITY);
+  for (int j = 0; j < l; ++j)
+    for (int i = 0; i < a - 1; ++i) {
+      e64[j * 256 + i] = m.edges[j * 255 + i];
+      e32[j * 256 + i] = (float)m.edges[j * 255 + i];
+    }
+  SOFA_CK(cudaMalloc(&ix->edges64, e64.size() * 8));
+  SOFA_CK(cudaMalloc(&ix->edges32, e32.size() * 4));
+  SOFA_CK(cudaMalloc(&ix->basis64, (size_t)LT * len * 8));
+  SOFA_CK(cudaMalloc(&ix->basis32, (size_t)LT * len * 4));
+  SOFA_CK(cudaMemcpyAsync(ix->edges64, e64.data(), e64.size() * 8, cudaMemcpyHostToDevice, st));
+  SOFA_CK(cudaMemcpyAsync(ix->edges32, e32.data(), e32.size() * 4, cudaMemcpyHostToDevice, st));
+  int* dpos = nullptr;
+  SOFA_CK(cudaMalloc(&dpos, SOFA_MAX_L * 4));
+  SOFA_CK(cudaMemcpyAsync(dpos, m.best_pos, SOFA_MAX_L * 4, cudaMemcpyHostToDevice, st));
+  k_basis_sel<<<(LT * len + 255) / 256, 256, 0, st>>>(dpos, l, LT, len, ix->basis64, ix->basis32);
+  cudaError_t e = cudaGetLastError();
+  g_launches.fetch_add(1);
+  cudaStreamSynchronize(st);
+  cudaFree(dpos);
+  if (e != cudaSuccess) return fail(SOFA_ECUDA, std::string("k_basis_sel: ") + cudaGetErrorString(e));
+  DevModel& dm = ix->dm;
+  dm.len = len;
+  dm.l = l;
+  dm.LT = LT;
+  dm.a = a;
+  dm.a_bits = 31 - __builtin_clz((unsigned)a);
+  dm.WS = ix->WS;
+  dm.basis32 = ix->basis32;
+  dm.basis64 = ix->basis64;
+  dm.edges32 = ix->edges32;
+  dm.edges64 = ix->edges64;
+  for (int j = 0; j < SOFA_MAX_L; ++j) dm.weights[j] = j < l ? (float)m.weights[j] : 0.f;
+  return SOFA_OK;
+}
+
+static int validate_model(const sofa_model& m) {
+  int rc = check_shape(m.len, m.l, m.alphabet);
+  if (rc) return rc;
+  for (int j = 0; j < m.l; ++j) {
+    if (m.best_pos[j] < 0 || m.best_pos[j] >= m.len + 2) return fail(SOFA_EINVAL, "model best_pos out of range");
+    for (int i = 1; i < m.alphabet - 1; ++i)
+      if (!(m.edges[j * 255 + i] >= m.edges[j * 255 + i - 1])) return fail(SOFA_EINVAL, "model edges not ascending");
+  }
+  return SOFA_OK;
+}
+
+}  // namespace sofa
+
+using namespace sofa;
+
+extern "C" {
+
+const char* sofa_last_error(void) { return g_err.c_str(); }
+
+int64_t sofa_launch_count(void) { return g_launches.load(); }
+
+int sofa_default_opts(sofa_build_opts* out) {
+  if (!out) return fail(SOFA_EINVAL, "out is NULL");
+  memset(out, 0, sizeof(*out));
+  out->sample_ratio = 0.01;
+  out->block_size = 256;
+  out->binning = SOFA_BINNING_EQUI_DEPTH;
+  return SOFA_OK;
+}
+
+int sofa_learn_model(const float* sample_dev, int64_t S, int32_t len, int32_t l, int32_t alphabet,
+                     const sofa_build_opts* opts, void* cuda_stream, sofa_model* out) {
+  g_err.clear();
+  int rc = check_shape(len, l, alphabet);
+  if (rc) return rc;
+  if (!sample_dev || !out) return fail(SOFA_EINVAL, "NULL pointer");
+  const int binning = opts ? opts->binning : SOFA_BINNING_EQUI_DEPTH;
+  const int cl = opts ? opts->candidate_limit : 0;
+  if (binning != SOFA_BINNING_EQUI_DEPTH && binning != SOFA_BINNING_EQUI_WIDTH) return fail(SOFA_EINVAL, "binning");
+  return learn_model_dev(sample_dev, S, len, l, alphabet, binning, cl, (cudaStream_t)cuda_stream, out);
+}
+
+void sofa_free(sofa_index* ix) {
+  if (!ix) return;
+  void* bufs[] = {ix->words, ix->stats, ix->perm, ix->env, ix->bkey, ix->basis32, ix->basis64, ix->edges32,
+                  ix->edges64, ix->gscratch, ix->qcounter, ix->dstats, ix->hq_dev, ix->hd_dev, ix->hi_dev};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  delete ix;
+}
+
+int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32_t alphabet,
+               const sofa_build_opts* opts_in, void* cuda_stream, sofa_index** out) {
+  g_err.clear();
+  if (!out) return fail(SOFA_EINVAL, "out is NULL");
+  *out = nullptr;
+  int rc = check_shape(len, l, alphabet);
+  if (rc) return rc;
+  sofa_build_opts opts;
+  sofa_default_opts(&opts);
+  if (opts_in) opts = *opts_in;
+  if (n < 0 || (n > 0 && !series_dev)) return fail(SOFA_EINVAL, "bad series / n");
+  if (n > 2147483647LL) return fail(SOFA_EINVAL, "n must fit int32 per shard");
+  if (!pow2(opts.block_size) || opts.block_size < 32 || opts.block_size > 8192)
+    return fail(SOFA_EINVAL, "block_size must be a power of two in [32, 8192]");
+  if (opts.binning != SOFA_BINNING_EQUI_DEPTH && opts.binning != SOFA_BINNING_EQUI_WIDTH)
+    return fail(SOFA_EINVAL, "binning");
+  const int64_t gn = opts.global_n > 0 ? opts.global_n : n;
+  if (opts.global_offset < 0 || opts.global_offset + n > gn) return fail(SOFA_EINVAL, "global_offset/global_n");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+
+  sofa_index* ix = new sofa_index();
+  ix->n = n;
+  ix->len = len;
+  ix->l = l;
+  ix->a = alphabet;
+  ix->B = opts.block_size;
+  ix->global_offset = opts.global_offset;
+  ix->global_n = gn;
+  ix->series = series_dev;
+  cudaGetDevice(&ix->device);
+  auto bail = [&](int code) {
+    sofa_free(ix);
+    return code;
+  };
+
+  // ---- a2: model
+  if (opts.model) {
+    const sofa_model& m = *opts.model;
+    if (m.len != len || m.l != l || m.alphabet != alphabet) return bail(fail(SOFA_EINVAL, "opts->model disagrees with (len, l, alphabet)"));
+    if ((rc = validate_model(m))) return bail(rc);
+    ix->model = m;
+  } else {
+    if (n == 0) return bail(fail(SOFA_EINVAL, "n = 0 needs opts->model"));
+    int64_t S = opts.sample_size > 0 ? opts.sample_size : (int64_t)llround(opts.sample_ratio * (double)gn);
+    const int64_t smin = opts.binning == SOFA_BINNING_EQUI_DEPTH ? alphabet : 2;
+    if (S < smin) S = smin;
+    if (S > gn) S = gn;
+    if (opts.binning == SOFA_BINNING_EQUI_DEPTH && S < alphabet)
+      return bail(fail(SOFA_EDEGENERATE, "equi-depth binning needs at least `alphabet` rows"));
+    // every sampled global row must be local
+    if ((0 * gn) / S < opts.global_offset || ((S - 1) * gn) / S >= opts.global_offset + n)
+      return bail(fail(SOFA_EINVAL, "sample rows are not all local: pass opts->model for a sharded build"));
+    float* smp = nullptr;
+    if (cudaMalloc(&smp, (size_t)S * len * 4) != cudaSuccess) return bail(fail(SOFA_ENOMEM, "sample buffer"));
+    k_gather_sample<<<148 * 8, 256, 0, st>>>(series_dev, S, gn, opts.global_offset, len, smp);
+    g_launches.fetch_add(1);
+    rc = learn_model_dev(smp, S, len, l, alphabet, opts.binning, opts.candidate_limit, st, &ix->model);
+    cudaStreamSynchronize(st);
+    cudaFree(smp);
+    if (rc) return bail(rc);
+  }
+  if ((rc = upload_model(ix->model, len, ix, st))) return bail(rc);
+  const int WS = ix->WS, B = ix->B;
+  ix->nb = (n + B - 1) / B;
+  if (cudaMalloc(&ix->qcounter, 64) != cudaSuccess || cudaMalloc(&ix->dstats, 16 * 8) != cudaSuccess)
+    return bail(fail(SOFA_ENOMEM, "counters"));
+  if (n == 0) {
+    cudaStreamSynchronize(st);
+    *out = ix;
+    return SOFA_OK;
+  }
+
+  // ---- a1 + a3: one pass over the series
+  uint8_t* words_u = nullptr;
+  float2* stats_u = nullptr;
+  uint64_t *keys_u = nullptr, *keys_s = nullptr;
+  int32_t* iota = nullptr;
+  void* tmp = nullptr;
+  auto freeall = [&]() {
+    void* ps[] = {words_u, stats_u, keys_u, keys_s, iota, tmp};
+    for (void* p : ps)
+      if (p) cudaFree(p);
+  };
+#define BCK(call)                                                              \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) {                                                   \
+      freeall();                                                               \
+      return bail(fail(e_ == cudaErrorMemoryAllocation ? SOFA_ENOMEM : SOFA_ECUDA, \
+                       std::string(#call) + ": " + cudaGetErrorString(e_)));   \
+    }                                                                          \
+  } while (0)
+  BCK(cudaMalloc(&words_u, (size_t)n * WS));
+  BCK(cudaMalloc(&stats_u, (size_t)n * 8));
+  BCK(cudaMalloc(&keys_u, (size_t)n * 8));
+  BCK(cudaMalloc(&keys_s, (size_t)n * 8));
+  BCK(cudaMalloc(&iota, (size_t)n * 4));
+  BCK(cudaMalloc(&ix->perm, (size_t)n * 4));
+  BCK(cudaMalloc(&ix->words, (size_t)n * WS));
+  BCK(cudaMalloc(&ix->stats, (size_t)n * 8));
+  BCK(cudaMalloc(&ix->env, (size_t)ix->nb * 2 * WS));
+  BCK(cudaMalloc(&ix->bkey, (size_t)ix->nb * 8));
+  if ((rc = launch_transform(series_dev, n, ix->dm, words_u, stats_u, keys_u, nullptr, nullptr, st))) {
+    freeall();
+    return bail(rc);
+  }
+  // ---- a4: sort by key (stable: equal keys keep row order), gather, envelopes
+  k_iota<<<148 * 8, 256, 0, st>>>(iota, n);
+  g_launches.fetch_add(1);
+  size_t tb = 0;
+  BCK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys_u, keys_s, iota, ix->perm, (int64_t)n, 0, 64, st));
+  BCK(cudaMalloc(&tmp, tb + 16));
+  BCK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys_u, keys_s, iota, ix->perm, (int64_t)n, 0, 64, st));
+  g_launches.fetch_add(1);
+  if ((rc = launch_gather(words_u, stats_u, ix->perm, n, WS, ix->words, ix->stats, st)) ||
+      (rc = launch_envelopes(ix->words, n, B, WS, keys_s, ix->env, ix->bkey, st))) {
+    freeall();
+    return bail(rc);
+  }
+  BCK(cudaStreamSynchronize(st));
+#undef BCK
+  freeall();
+  *out = ix;
+  return SOFA_OK;
+}
+
+int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, const float* bsf_init_dev,
+             float* out_dist_dev, int64_t* out_idx_dev, sofa_knn_stats* stats, void* cuda_stream) {
+  g_err.clear();
+  if (!ix) return fail(SOFA_EINVAL, "index is NULL");
+  if (q < 1) return fail(SOFA_EINVAL, "q must be >= 1");
+  if (k < 1 || k > SOFA_MAX_K) return fail(SOFA_EINVAL, "k must be in [1, 128]");
+  if (k > ix->global_n) return fail(SOFA_EINVAL, "k exceeds the number of series");
+  if (!queries_dev || !out_dist_dev || !out_idx_dev) return fail(SOFA_EINVAL, "NULL pointer");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (stats) SOFA_CK(cudaMemsetAsync(ix->dstats, 0, 16 * 8, st));
+  int rc;
+  if (ix->n == 0)
+    rc = launch_fill_pad(out_dist_dev, out_idx_dev, (int64_t)q * k, st);
+  else
+    rc = launch_query(ix, queries_dev, q, k, bsf_init_dev, out_dist_dev, out_idx_dev, st);
+  if (rc) return rc;
+  if (stats) {
+    unsigned long long h[16] = {};
+    SOFA_CK(cudaMemcpyAsync(h, ix->dstats, 16 * 8, cudaMemcpyDeviceToHost, st));
+    SOFA_CK(cudaStreamSynchronize(st));
+    stats->queries = q;
+    stats->blocks_total = (int64_t)h[1];
+    stats->blocks_survived = (int64_t)h[2];
+    stats->words_scanned = (int64_t)h[3];
+    stats->candidates = (int64_t)h[4];
+    stats->refined = (int64_t)h[5];
+    stats->abandoned = (int64_t)h[6];
+  }
+  return SOFA_OK;
+}
+
+int sofa_knn_host(sofa_index* ix, const float* queries_host, int32_t q, int32_t k, float* out_dist_host,
+                  int64_t* out_idx_host, sofa_knn_stats* stats, void* cuda_stream) {
+  g_err.clear();
+  if (!ix || !queries_host || !out_dist_host || !out_idx_host || q < 1 || k < 1 || k > SOFA_MAX_K)
+    return fail(SOFA_EINVAL, "bad arguments");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int64_t need = (int64_t)q * (ix->len > k ? ix->len : k);
+  if (ix->h_cap < need) {
+    if (ix->hq_dev) cudaFree(ix->hq_dev);
+    if (ix->hd_dev) cudaFree(ix->hd_dev);
+    if (ix->hi_dev) cudaFree(ix->hi_dev);
+    ix->hq_dev = nullptr;
+    ix->hd_dev = nullptr;
+    ix->hi_dev = nullptr;
+    SOFA_CK(cudaMalloc(&ix->hq_dev, need * 4));
+    SOFA_CK(cudaMalloc(&ix->hd_dev, need * 4));
+    SOFA_CK(cudaMalloc(&ix->hi_dev, need * 8));
+    ix->h_cap = need;
+  }
+  SOFA_CK(cudaMemcpyAsync(ix->hq_dev, queries_host, (size_t)q * ix->len * 4, cudaMemcpyHostToDevice, st));
+  int rc = sofa_knn(ix, ix->hq_dev, q, k, nullptr, ix->hd_dev, ix->hi_dev, stats, cuda_stream);
+  if (rc) return rc;
+  SOFA_CK(cudaMemcpyAsync(out_dist_host, ix->hd_dev, (size_t)q * k * 4, cudaMemcpyDeviceToHost, st));
+  SOFA_CK(cudaMemcpyAsync(out_idx_host, ix->hi_dev, (size_t)q * k * 8, cudaMemcpyDeviceToHost, st));
+  SOFA_CK(cudaStreamSynchronize(st));
+  return SOFA_OK;
+}
+
+int sofa_merge_topk(const float* dist_dev, const int64_t* idx_dev, int32_t parts, int32_t q, int32_t k,
+                    float* out_dist_dev, int64_t* out_idx_dev, void* cuda_stream) {
+  g_err.clear();
+  if (parts < 1 || parts > 64) return fail(SOFA_EINVAL, "parts must be in [1, 64]");
+  if (q < 1 || k < 1 || k > SOFA_MAX_K) return fail(SOFA_EINVAL, "bad q / k");
+  if (!dist_dev || !idx_dev || !out_dist_dev || !out_idx_dev) return fail(SOFA_EINVAL, "NULL pointer");
+  return launch_merge(dist_dev, idx_dev, parts, q, k, out_dist_dev, out_idx_dev, (cudaStream_t)cuda_stream);
+}
+
+int sofa_get_model(const sofa_index* ix, sofa_model* out) {
+  if (!ix || !out) return fail(SOFA_EINVAL, "NULL pointer");
+  *out = ix->model;
+  return SOFA_OK;
+}
+
+int sofa_transform(const float* series_dev, int64_t n, const sofa_model* model, double* out_values_dev,
+                   uint8_t* out_words_dev, void* cuda_stream) {
+  g_err.clear();
+  if (!model || n < 0 || (n > 0 && !series_dev)) return fail(SOFA_EINVAL, "bad arguments");
+  int rc = validate_model(*model);
+  if (rc) return rc;
+  sofa_index tmp;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  rc = upload_model(*model, model->len, &tmp, st);
+  if (!rc) rc = launch_transform(series_dev, n, tmp.dm, nullptr, nullptr, nullptr, out_values_dev, out_words_dev, st);
+  cudaStreamSynchronize(st);
+  void* ps[] = {tmp.basis32, tmp.basis64, tmp.edges32, tmp.edges64};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  return rc;
+}
+
+int sofa_get_info(const sofa_index* ix, sofa_index_info* out) {
+  if (!ix || !out) return fail(SOFA_EINVAL, "NULL pointer");
+  out->n = ix->n;
+  out->n_blocks = ix->nb;
+  out->global_offset = ix->global_offset;
+  out->global_n = ix->global_n;
+  out->len = ix->len;
+  out->l = ix->l;
+  out->alphabet = ix->a;
+  out->block_size = ix->B;
+  out->word_stride = ix->WS;
+  return SOFA_OK;
+}
+
+int sofa_export_index(const sofa_index* ix, uint8_t* words_sorted_dev, int32_t* perm_dev, uint8_t* env_dev,
+                      uint64_t* block_keys_dev, void* cuda_stream) {
+  if (!ix) return fail(SOFA_EINVAL, "NULL index");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (ix->n == 0) return SOFA_OK;
+  if (words_sorted_dev)
+    SOFA_CK(cudaMemcpyAsync(words_sorted_dev, ix->words, (size_t)ix->n * ix->WS, cudaMemcpyDeviceToDevice, st));
+  if (perm_dev) SOFA_CK(cudaMemcpyAsync(perm_dev, ix->perm, (size_t)ix->n * 4, cudaMemcpyDeviceToDevice, st));
+  if (env_dev)
+    SOFA_CK(cudaMemcpyAsync(env_dev, ix->env, (size_t)ix->nb * 2 * ix->WS, cudaMemcpyDeviceToDevice, st));
+  if (block_keys_dev)
+    SOFA_CK(cudaMemcpyAsync(block_keys_dev, ix->bkey, (size_t)ix->nb * 8, cudaMemcpyDeviceToDevice, st));
+  SOFA_CK(cudaStreamSynchronize(st));
+  return SOFA_OK;
+}
+
+}  // extern "C"

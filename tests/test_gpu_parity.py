@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU float64 oracle on the same seeded
+inputs.  Acceptance (BASELINE.json north_star): neighbour indices exact except ties within 1e-5
+relative distance; distances within 1e-4 relative; SFA symbols bit-exact except values within
+1e-5 of a bin edge; the learned model equal to the oracle's (best_l identical, edges within
+float32 rounding)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import sofa_oracle as O
+from paper_2411_17483_b200 import datagen
+from paper_2411_17483_b200.index import SofaIndex, learn_model, merge_topk, transform
+
+pytestmark = pytest.mark.gpu
+
+DIST_RTOL = 1e-4
+TIE_RTOL = 1e-5
+
+
+def _data(w, device="cuda"):
+    x = datagen.generate_rows(w, 0, w.n_series, device=device)
+    q = datagen.generate_queries(w, device=device, data=x)
+    return x, q
+
+
+def assert_knn_parity(d_gpu, i_gpu, d_or, i_or, data_np=None, queries_np=None):
+    """indices exact except ties within TIE_RTOL; distances within DIST_RTOL relative."""
+    d_gpu = np.asarray(d_gpu, dtype=np.float64)
+    assert d_gpu.shape == d_or.shape
+    fin = np.isfinite(d_or)
+    assert np.array_equal(np.isfinite(d_gpu), fin)
+    np.testing.assert_allclose(d_gpu[fin], d_or[fin], rtol=DIST_RTOL, atol=1e-6)
+    bad = (i_gpu != i_or) & fin
+    for q, r in zip(*np.nonzero(bad)):
+        # allowed only as a tie: the GPU's neighbour is within TIE_RTOL of the oracle's rank-r distance
+        ref = d_or[q, r]
+        if data_np is not None:
+            xh, _, _, _ = O.znorm(data_np[i_gpu[q, r]:i_gpu[q, r] + 1])
+            qh, _, _, _ = O.znorm(queries_np[q:q + 1])
+            true_d = math.sqrt(O.sq_dists_direct(xh, qh[0])[0])
+        else:
+            true_d = d_gpu[q, r]
+        assert abs(true_d - ref) <= TIE_RTOL * max(ref, 1e-12) + 1e-7, (q, r, i_gpu[q, r], i_or[q, r], true_d, ref)
+
+
+# ------------------------------------------------------------------------------------- a2 model
+@pytest.mark.parametrize("kind,n,l,binning", [("cfg1", 256, 16, "equi-depth"), ("cfg3", 256, 16, "equi-depth"),
+                                              ("cfg1", 256, 16, "equi-width"), ("cfg5", 1024, 32, "equi-depth"),
+                                              ("cfg1", 64, 8, "equi-depth")])
+def test_model_parity(kind, n, l, binning):
+    w = datagen.scaled(datagen.WORKLOADS[kind], 6000, 4, length=n, l=l)
+    x = datagen.generate_rows(w, 0, w.n_series, device="cuda")
+    S = 3000
+    idx = O.sample_indices(w.n_series, S)
+    sample = x[torch.as_tensor(idx, device="cuda")]
+    mg = learn_model(sample, l, 256, binning=binning)
+    mo = O.learn_model(sample.cpu().numpy(), l, 256, binning=binning)
+    assert np.array_equal(mg["best_pos"], mo["best_pos"])
+    np.testing.assert_array_equal(mg["weights"], mo["weights"])
+    np.testing.assert_allclose(mg["edges"], mo["edges"], rtol=1e-7, atol=1e-9)
+    # the index's own model (learned from the strided sample inside sofa_build) is the same model
+    ix = SofaIndex(x, l=l, alphabet=256, sample_size=S, binning=binning)
+    mi = ix.model
+    assert np.array_equal(mi["best_pos"], mo["best_pos"])
+    np.testing.assert_allclose(mi["edges"], mo["edges"], rtol=1e-7, atol=1e-9)
+
+
+# ------------------------------------------------------------------------------------- a1 + a3 transform
+def _edge_exempt(vals, model):
+    """True where the oracle value lies within 1e-5 (relative above 1) of a bin edge."""
+    ex = np.zeros(vals.shape, dtype=bool)
+    for j in range(vals.shape[1]):
+        e = model["edges"][j]
+        pos = np.searchsorted(e, vals[:, j])
+        for cand in (pos - 1, pos):
+            c = np.clip(cand, 0, len(e) - 1)
+            ex[:, j] |= np.abs(vals[:, j] - e[c]) <= 1e-5 * np.maximum(1.0, np.abs(e[c]))
+    return ex
+
+
+@pytest.mark.parametrize("kind,n,l", [("cfg1", 256, 16), ("cfg3", 256, 16), ("cfg5", 1024, 32), ("cfg1", 128, 24),
+                                      ("cfg3", 96, 40)])
+def test_transform_parity(kind, n, l):
+    w = datagen.scaled(datagen.WORKLOADS[kind], 40_000, 4, length=n, l=l)
+    x = datagen.generate_rows(w, 0, w.n_series, device="cuda")
+    xn = x.cpu().numpy()
+    mo = O.learn_model(xn[O.sample_indices(w.n_series, 4000)], l, 256)
+    vals, words = transform(x, mo)
+    vo = O.project(xn, mo)
+    err = np.abs(vals.cpu().numpy() - vo)
+    assert err.max() < 5e-6, err.max()
+    so = O.quantize(vo, mo)
+    sg = words.cpu().numpy().astype(np.int64)
+    mism = (so != sg) & ~_edge_exempt(vo, mo)
+    assert mism.sum() == 0, (mism.sum(), np.argwhere(mism)[:5])
+    assert np.all(np.abs(so - sg) <= 1)
+
+
+def test_index_invariants():
+    w = datagen.scaled(datagen.WORKLOADS["cfg1"], 50_000 + 77, 4)
+    x = datagen.generate_rows(w, 0, w.n_series, device="cuda")
+    ix = SofaIndex(x, sample_size=5000, block_size=256)
+    inf = ix.info
+    assert inf["n_blocks"] == (w.n_series + 255) // 256
+    ex = ix.export()
+    perm = ex["perm"].cpu().numpy()
+    assert np.array_equal(np.sort(perm), np.arange(w.n_series))
+    _, words = transform(x, ix.raw_model)
+    wsorted = ex["words"][:, :16].cpu().numpy()
+    assert np.array_equal(wsorted, words.cpu().numpy()[perm])
+    # keys: 2-bit interleave of the first 16 positions, MSB first -> sorted order non-decreasing
+    s = wsorted.astype(np.uint64)
+    key = np.zeros(len(s), dtype=np.uint64)
+    for r in range(2):
+        for p in range(16):
+            key = (key << np.uint64(2)) | ((s[:, p] >> np.uint64(6 - 2 * r)) & np.uint64(3))
+    assert np.all(np.diff(key.astype(np.float64)) >= 0) or np.all(key[1:] >= key[:-1])
+    env = ex["env"].cpu().numpy()
+    for b in range(inf["n_blocks"]):
+        blk = wsorted[b * 256:(b + 1) * 256]
+        assert np.array_equal(env[b, 0, :16], blk.min(axis=0))
+        assert np.array_equal(env[b, 1, :16], blk.max(axis=0))
+    assert np.array_equal(ex["block_keys"].cpu().numpy().astype(np.uint64), key[::256])
+
+
+# ------------------------------------------------------------------------------------- k-NN parity
+@pytest.mark.parametrize("kind,N,n,l,k,Q", [
+    ("cfg1", 100_000, 256, 16, 1, 100),     # BJ configs[0] at full size
+    ("cfg2", 200_000, 256, 16, 1, 200),     # noisy members sigma 0.1
+    ("cfg3", 60_000, 256, 16, 1, 40),       # high frequency (low pruning)
+    ("cfg4", 200_000, 256, 16, 1, 150),     # sigma mix 0.01 / 0.1 / 1.0
+    ("cfg5", 40_000, 1024, 32, 10, 40),     # mixed n=1024, l=32, 10-NN
+    ("cfg1", 30_000, 256, 16, 10, 50),
+    ("cfg3", 20_000, 128, 16, 5, 30),
+])
+def test_knn_parity(kind, N, n, l, k, Q):
+    w = datagen.scaled(datagen.WORKLOADS[kind], N, Q, length=n, l=l, k=k)
+    x, q = _data(w)
+    ix = SofaIndex(x, l=l, alphabet=256, sample_size=datagen.default_sample_size(w))
+    d, i, st = ix.knn(q, k, stats=True)
+    torch.cuda.synchronize()
+    xn, qn = x.cpu().numpy(), q.cpu().numpy()
+    do, io = O.knn_bruteforce(xn, qn, k)
+    assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, xn, qn)
+    assert st["queries"] == Q and st["refined"] >= Q * min(k, 1)
+    if kind in ("cfg2",):
+        assert st["refined"] < 0.01 * N * Q          # pruning works on noisy-member queries
+
+
+@pytest.mark.parametrize("B", [32, 64, 1024, 4096])
+def test_result_invariant_to_block_size(B):
+    w = datagen.scaled(datagen.WORKLOADS["cfg4"], 40_000, 60)
+    x, q = _data(w)
+    ref = SofaIndex(x, sample_size=4000, block_size=256).knn(q, 3)
+    got = SofaIndex(x, sample_size=4000, block_size=B).knn(q, 3)
+    assert torch.equal(ref[1], got[1]) and torch.equal(ref[0], got[0])
+
+
+@pytest.mark.parametrize("parts", [2, 3, 5])
+def test_sharded_merge_equals_unsharded(parts):
+    w = datagen.scaled(datagen.WORKLOADS["cfg1"], 30_011, 40)
+    x, q = _data(w)
+    k = 4
+    full = SofaIndex(x, sample_size=3000)
+    d0, i0 = full.knn(q, k)
+    model = full.raw_model
+    ds, is_ = [], []
+    for r in range(parts):
+        a, b = datagen.shard_range(w.n_series, r, parts)
+        sh = x[a:b].contiguous()
+        ix = SofaIndex(sh, model=model, global_offset=a, global_n=w.n_series)
+        d, i = ix.knn(q, k)
+        ds.append(d)
+        is_.append(i)
+        del ix
+    md, mi = merge_topk(torch.stack(ds), torch.stack(is_))
+    assert torch.equal(mi, i0) and torch.equal(md, d0)
+
+
+def test_bsf_init_prunes_without_changing_results():
+    w = datagen.scaled(datagen.WORKLOADS["cfg2"], 50_000, 64)
+    x, q = _data(w)
+    ix = SofaIndex(x, sample_size=5000)
+    d0, i0, s0 = ix.knn(q, 1, stats=True)
+    bsf = (d0[:, 0] ** 2) * 1.001
+    d1, i1, s1 = ix.knn(q, 1, bsf_init=bsf.contiguous(), stats=True)
+    assert torch.equal(i0, i1)
+    tight = (d0[:, 0] ** 2) * 0.5          # bound below the true NN: nothing may be returned
+    d2, i2 = ix.knn(q, 1, bsf_init=tight.contiguous())
+    assert bool((i2 == -1).all()) and bool(torch.isinf(d2).all())
+
+
+# ------------------------------------------------------------------------------------- edge cases
+def test_edge_cases_small_and_degenerate():
+    rng = np.random.default_rng(5)
+    base = np.cumsum(rng.normal(size=(300, 32)), axis=1).astype(np.float32)
+    base[17] = base[3]                      # exact duplicate -> tie to the smaller index
+    base[40] = 7.0                          # constant series -> zero vector
+    base[41] = base[41] * 1000 + 55.0       # large offset/scale -> same z-normalised shape
+    x = torch.from_numpy(base).cuda()
+    ix = SofaIndex(x, l=8, alphabet=16, sample_size=300, block_size=32)
+    qs = torch.from_numpy(base[[3, 40, 41, 100]]).cuda()
+    d, i = ix.knn(qs, 3)
+    do, io = O.knn_bruteforce(base, base[[3, 40, 41, 100]], 3)
+    assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, base, base[[3, 40, 41, 100]])
+    assert i[0, 0].item() == 3 and i[0, 1].item() == 17 and d[0, 0].item() == 0.0
+    # k = N: the full sorted list
+    small = x[:37].contiguous()
+    ixs = SofaIndex(small, l=4, alphabet=4, sample_size=37, block_size=32)
+    d, i = ixs.knn(qs, 37)
+    do, io = O.knn_bruteforce(base[:37], base[[3, 40, 41, 100]], 37)
+    assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, base[:37], base[[3, 40, 41, 100]])
+
+
+def test_single_series_and_padding_and_short_len():
+    rng = np.random.default_rng(6)
+    x = torch.from_numpy(rng.normal(size=(1, 8)).astype(np.float32)).cuda()
+    ix = SofaIndex(x, l=3, alphabet=2, sample_size=2, binning="equi-width")
+    d, i = ix.knn(x, 1)
+    assert i.item() == 0 and d.item() == 0.0
+    x4 = torch.from_numpy(rng.normal(size=(500, 4)).astype(np.float32)).cuda()
+    ix4 = SofaIndex(x4, l=3, alphabet=4, sample_size=100, block_size=32)
+    q4 = torch.from_numpy(rng.normal(size=(7, 4)).astype(np.float32)).cuda()
+    d, i = ix4.knn(q4, 2)
+    do, io = O.knn_bruteforce(x4.cpu().numpy(), q4.cpu().numpy(), 2)
+    assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, x4.cpu().numpy(), q4.cpu().numpy())
+    # empty shard with a model pads
+    m = ix4.raw_model
+    empty = torch.empty(0, 4, dtype=torch.float32, device="cuda")
+    ixe = SofaIndex(empty, l=3, alphabet=4, model=m, global_n=500)
+    d, i = ixe.knn(q4, 2)
+    assert bool((i == -1).all()) and bool(torch.isinf(d).all())
+
+
+def test_host_path_equals_device_path():
+    w = datagen.scaled(datagen.WORKLOADS["cfg2"], 20_000, 32)
+    x, q = _data(w)
+    ix = SofaIndex(x, sample_size=2000)
+    d, i = ix.knn(q, 2)
+    hd, hi = ix.knn_host(q.cpu().numpy(), 2)
+    assert np.array_equal(hi, i.cpu().numpy()) and np.array_equal(hd, d.cpu().numpy())
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_sampled():
+    """BJ configs[1] at full size (10M x 256, 1000 noisy queries) in the bench's launch
+    configuration: every query's 1-NN is its source member (known answer for sigma=0.1,
+    SURVEY 8(c)), and 3 sampled queries match the oracle's brute force over all 10M rows."""
+    w = datagen.WORKLOADS["cfg2"]
+    x = datagen.generate_rows(w, 0, w.n_series, device="cuda")
+    q = datagen.generate_queries(w, device="cuda", data=x)
+    ix = SofaIndex(x, sample_size=datagen.default_sample_size(w))
+    d, i = ix.knn(q, 1)
+    src = datagen.query_sources(w)
+    assert np.array_equal(i[:, 0].cpu().numpy(), src)
+    pick = [0, 499, 998]
+    qn = q[pick].cpu().numpy()
+    best_d = np.full(3, np.inf)
+    best_i = np.full(3, -1)
+    for s in range(0, w.n_series, 1 << 20):
+        chunk = x[s:s + (1 << 20)].cpu().numpy()
+        dd, ii = O.knn_bruteforce(chunk, qn, 1)
+        better = dd[:, 0] < best_d
+        best_d[better] = dd[better, 0]
+        best_i[better] = ii[better, 0] + s
+    np.testing.assert_allclose(d[pick, 0].cpu().numpy(), best_d, rtol=DIST_RTOL)
+    assert np.array_equal(i[pick, 0].cpu().numpy(), best_i)
