@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native SOFA exact k-NN path (BASELINE.json metric: exact k-NN queries/sec).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl sofa|reference]
+
+A step = one exact k-NN batch (all Q queries of the config) through libsofa's query kernel
+(a5-a8) on an index built over the synthetic dataset (a1-a4, timed separately as `build`), plus
+the NCCL all-gather + merge kernel (a9) when N > 1.  Data and queries are resident in HBM when
+the timed region starts; L2 is flushed (512 MB write) between timed steps; each step is timed with
+CUDA events on the launching stream; max over ranks.  N > 1 shards the same dataset over the
+ranks (strong scaling).  `e2e` repeats the measurement through the host-buffer C call
+(sofa_knn_host: pinned host queries in, host results out).  `--impl reference` times the CPU
+float64 oracle (the reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2411_17483_b200 import datagen  # noqa: E402
+
+METRIC = "exact k-NN queries/sec"
+UNIT = "queries/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="cfg2", choices=sorted(datagen.WORKLOADS))
+    p.add_argument("--impl", default="sofa", choices=["sofa", "reference"])
+    p.add_argument("--n-series", type=int, default=0, help="override N (debug only; changes the workload)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev, self.rows, self.proc = dev, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.dev), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(w, rows: int, nq: int, x_host: np.ndarray | None = None, q_host: np.ndarray | None = None):
+    """Time the CPU oracle (brute force, float64) for nq queries over `rows` rows; returns (q/s
+    extrapolated to the full N, seconds, sample description)."""
+    from oracle import sofa_oracle as O
+    if x_host is None:
+        x_host = datagen.generate_rows(w, 0, rows).numpy()
+    if q_host is None:
+        q_host = datagen.generate_queries(datagen.scaled(w, w.n_series, nq)).numpy()[:nq]
+    t0 = time.perf_counter()
+    O.knn_bruteforce(x_host, q_host, w.k)
+    dt = time.perf_counter() - t0
+    per_query_full = dt / nq * (w.n_series / rows)
+    return 1.0 / per_query_full, dt, f"{nq} queries x first {rows:,} of {w.n_series:,} rows, brute force float64, " \
+                                     f"time extrapolated linearly in N"
+
+
+def run_reference(a, w):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch as _t
+    _t.set_num_threads(cores())
+    rows = min(w.n_series, 250_000 if w.length <= 256 else 60_000)
+    nq = 4
+    x = datagen.generate_rows(w, 0, rows).numpy()
+    qh = datagen.generate_queries(datagen.scaled(w, w.n_series, nq) if w.query_kind == "independent"
+                                  else datagen.scaled(w, rows, nq), data=None).numpy()[:nq]
+    vals = []
+    for s in range(a.warmup + a.steps):
+        v, dt, desc = oracle_sample(w, rows, nq, x, qh)
+        if s >= a.warmup:
+            vals.append((v, dt))
+    v = statistics.median([x[0] for x in vals])
+    ms = statistics.median([x[1] for x in vals]) * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "n_series": w.n_series, "length": w.length, "l": w.l, "alphabet": w.alphabet,
+                       "k": w.k, "queries": w.n_queries},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores(), "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def flush_l2(buf):
+    buf.zero_()
+
+
+def main():
+    a = parse()
+    w = datagen.WORKLOADS[a.config]
+    if a.n_series:
+        w = datagen.scaled(w, a.n_series, w.n_queries)
+    if a.impl == "reference":
+        run_reference(a, w)
+        return
+
+    from paper_2411_17483_b200 import sofa as S
+    from paper_2411_17483_b200.index import SofaIndex
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    lo, hi = datagen.shard_range(w.n_series, rank, world)
+
+    # ---------------------------------------------------------------- data (resident in HBM)
+    x = datagen.generate_rows(w, lo, hi, device=dev)
+    q = datagen.generate_queries(w, device=dev, data=x if world == 1 else None, data_offset=lo)
+    torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- build (a1-a4), timed separately
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    if world == 1:
+        ix = SofaIndex(x, l=w.l, alphabet=w.alphabet, sample_size=datagen.default_sample_size(w))
+        knn = lambda qq: ix.knn(qq, w.k)  # noqa: E731
+        index = ix
+    else:
+        from paper_2411_17483_b200.distributed import ShardedSofa
+        sh = ShardedSofa(x, lo, w.n_series, l=w.l, alphabet=w.alphabet, sample_size=datagen.default_sample_size(w))
+        knn = lambda qq: sh.knn(qq, w.k)  # noqa: E731
+        index = sh.index
+    e1.record()
+    torch.cuda.synchronize()
+    build_ms = e0.elapsed_time(e1)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    l2 = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(a.warmup):
+        knn(q)
+    torch.cuda.synchronize()
+    _, _, st = index.knn(q, w.k, stats=True)  # pruning statistics of this shard (same work as a step)
+
+    # ---------------------------------------------------------------- timed steps
+    times = []
+    launches0 = S.sofa_launch_count()
+    with Clocks(local) as clk:
+        for s in range(a.steps):
+            flush_l2(l2)
+            barrier()
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            d, i = knn(q)
+            s1.record()
+            torch.cuda.synchronize()
+            barrier()
+            times.append(s0.elapsed_time(s1))
+        # keep sampling clocks for a short sustained run of the same step (no timing taken)
+        t_end = time.time() + 1.0
+        while time.time() < t_end:
+            knn(q)
+        torch.cuda.synchronize()
+    launches = S.sofa_launch_count() - launches0
+    tot_ms = max_over_ranks(sum(times))
+    ms_per_step = tot_ms / a.steps
+    value = w.n_queries * a.steps / (tot_ms / 1e3)
+
+    # ---------------------------------------------------------------- roofline of the query kernel
+    hbm, peak_kind = peaks()
+    l_b, n_b = w.l, 4 * w.length
+    alg_bytes = (st["blocks_total"] * 2 * l_b + st["words_scanned"] * l_b + st["refined"] * n_b
+                 + st["queries"] * n_b)
+    kern_ms = statistics.median(times)   # at N=1 the step is the query kernel (+ a 4-byte memset)
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{a.config}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+
+    # ---------------------------------------------------------------- e2e through the host C call
+    e2e = None
+    if not a.no_e2e:
+        qh = torch.empty(q.shape, dtype=torch.float32, pin_memory=True)
+        qh.copy_(q)
+        qhn = qh.numpy()
+        od = torch.empty(w.n_queries, w.k, dtype=torch.float32, pin_memory=True).numpy()
+        oi = torch.empty(w.n_queries, w.k, dtype=torch.int64, pin_memory=True).numpy()
+        et = []
+        for s in range(a.warmup + a.steps):
+            flush_l2(l2)
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if world == 1:
+                index.knn_host(qhn, w.k, out=(od, oi))
+            else:
+                qd = qh.to(dev, non_blocking=True)
+                dd, ii = knn(qd)
+                dd.cpu(), ii.cpu()
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            barrier()
+            if s >= a.warmup:
+                et.append(dt)
+        e_tot = max_over_ranks(sum(et))
+        e2e = {"value": w.n_queries * a.steps / e_tot, "unit": UNIT,
+               "h2d_bytes_per_step": int(w.n_queries * w.length * 4),
+               "d2h_bytes_per_step": int(w.n_queries * w.k * 12)}
+
+    # ---------------------------------------------------------------- cpu baseline (oracle), rank 0, N=1
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        torch.set_num_threads(cores())
+        rows = min(w.n_series, 1_000_000 if w.length <= 256 else 250_000)
+        nq = 4
+        xs = x[:rows].cpu().numpy()
+        qs = q[:nq].cpu().numpy()
+        v, dt, desc = oracle_sample(w, rows, nq, xs, qs)
+        cpu = {"value": v, "unit": UNIT, "cores": cores(), "kind": "oracle", "sample": desc, "seconds": dt}
+
+    if rank == 0:
+        N = w.n_series
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": w.name, "n_series": N, "length": w.length, "l": w.l, "alphabet": w.alphabet,
+                       "k": w.k, "queries": w.n_queries, "block_size": 256,
+                       "sample_size": datagen.default_sample_size(w),
+                       "l2": "flushed between timed steps (512 MB write)", "parallelism": f"shard{world}"},
+            "prune": {"series": 1.0 - st["refined"] / (st["queries"] * (hi - lo)),
+                      "block": 1.0 - st["blocks_survived"] / max(1, st["blocks_total"]),
+                      "refined_per_query": st["refined"] / st["queries"],
+                      "words_scanned_per_query": st["words_scanned"] / st["queries"]},
+            "build": {"ms": build_ms, "gb_per_s_series_read": (hi - lo) * w.length * 4 / (build_ms / 1e3) / 1e9},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "k_query (a5-a8 fused)", "algorithmic_bytes_per_launch": alg_bytes,
+                         "kernel_ms": kern_ms},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    index.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -202,6 +202,7 @@ __device__ void refine_candidates(const QArgs& A, QShared& S, unsigned long long
         const int i = s_wi[w];
         if (i < 0) continue;
         const float d = s_wd[w];
+        if (d > S.bsf_init) continue;  // above the caller's bound: never part of the answer
         const int n = S.tkn;
         if (n < k || d < s_tkd[n - 1] || (d == s_tkd[n - 1] && i < s_tki[n - 1])) {
           int p = n < k ? n : k - 1;

@@ -1,0 +1,99 @@
+"""One process per GPU: dataset sharding, the global MCB model (C1) and the top-k exchange (C4).
+
+SURVEY 8(e): series are independent, so each rank holds a contiguous shard (datagen.shard_range)
+and builds its own index with the GLOBAL model; a query batch is replicated on every rank, each
+rank returns its local top-k with global indices, and an all-gather (NCCL over NVLink on a GPU
+box) followed by the libsofa min-merge kernel (a9) gives the global answer.  The exchange is
+tiny (P x Q x k x 12 bytes), so it is latency-bound.
+
+The collective plumbing is written against torch.distributed only; the compute steps (learning,
+local k-NN, merge) are passed in, so the same host logic runs over gloo on CPU in the tests
+(with oracle functions injected by the test) and over NCCL with the CUDA kernels in the product.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def global_sample_indices(global_n: int, S: int) -> np.ndarray:
+    """Alg. 1 sample(X, r) as strided global rows floor(j * N / S) (reading 6)."""
+    return (np.arange(S, dtype=np.int64) * global_n) // S
+
+
+def gather_global_sample(shard: torch.Tensor, global_offset: int, global_n: int, S: int, group=None) -> torch.Tensor:
+    """Every rank contributes the sample rows that fall in its shard; all ranks receive the
+    S x len sample in j order (ranks hold contiguous ranges, so rank order is j order)."""
+    idx = global_sample_indices(global_n, S)
+    mine = idx[(idx >= global_offset) & (idx < global_offset + shard.shape[0])] - global_offset
+    local = shard[torch.as_tensor(mine, device=shard.device)] if len(mine) else shard[:0]
+    world = dist.get_world_size(group)
+    counts = [torch.zeros(1, dtype=torch.int64, device=shard.device) for _ in range(world)]
+    dist.all_gather(counts, torch.tensor([local.shape[0]], dtype=torch.int64, device=shard.device), group=group)
+    counts = [int(c.item()) for c in counts]
+    mx = max(counts)
+    pad = torch.zeros(mx, shard.shape[1], dtype=shard.dtype, device=shard.device)
+    pad[:local.shape[0]] = local
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    out = torch.cat([p[:c] for p, c in zip(parts, counts)])
+    assert out.shape[0] == S
+    return out
+
+
+def broadcast_model_bytes(model_bytes: bytes | None, device, group=None, src: int = 0) -> bytes:
+    """C1: rank `src` learned the model; every rank gets the same plain-data bytes."""
+    n = torch.tensor([len(model_bytes) if model_bytes is not None else 0], dtype=torch.int64, device=device)
+    dist.broadcast(n, src=src, group=group)
+    buf = torch.zeros(int(n.item()), dtype=torch.uint8, device=device)
+    if dist.get_rank(group) == src:
+        buf.copy_(torch.frombuffer(bytearray(model_bytes), dtype=torch.uint8).to(device))
+    dist.broadcast(buf, src=src, group=group)
+    return bytes(buf.cpu().numpy().tobytes())
+
+
+def allgather_topk(dist_local: torch.Tensor, idx_local: torch.Tensor, group=None):
+    """C4: every rank's (Q, k) local top-k -> (P, Q, k) on every rank."""
+    world = dist.get_world_size(group)
+    dl = [torch.empty_like(dist_local) for _ in range(world)]
+    il = [torch.empty_like(idx_local) for _ in range(world)]
+    dist.all_gather(dl, dist_local.contiguous(), group=group)
+    dist.all_gather(il, idx_local.contiguous(), group=group)
+    return torch.stack(dl), torch.stack(il)
+
+
+def sharded_knn(queries, k, local_knn, merge, group=None):
+    """Local k-NN on this rank's shard, all-gather, min-merge (a9)."""
+    d, i = local_knn(queries, k)
+    D, I = allgather_topk(d, i, group)
+    return merge(D, I)
+
+
+# ------------------------------------------------------------------------------ product wiring
+class ShardedSofa:
+    """Product path: libsofa on this rank's GPU, NCCL for C1 / C4."""
+
+    def __init__(self, shard: torch.Tensor, global_offset: int, global_n: int, l: int = 16, alphabet: int = 256,
+                 sample_size: int = 0, block_size: int = 256, group=None):
+        from . import sofa as S
+        from .index import SofaIndex, learn_model  # noqa: F401
+
+        self.group = group
+        S_ = sample_size or max(alphabet, int(round(0.01 * global_n)))
+        sample = gather_global_sample(shard, global_offset, global_n, S_, group)
+        mb = None
+        if dist.get_rank(group) == 0:
+            m = S.sofa_learn_model(sample, S_, shard.shape[1], l, alphabet)
+            mb = ctypes.string_at(ctypes.addressof(m), ctypes.sizeof(m))
+        mb = broadcast_model_bytes(mb, shard.device, group)
+        model = S.sofa_model.from_buffer_copy(mb)
+        del sample
+        self.index = SofaIndex(shard, l=l, alphabet=alphabet, block_size=block_size, model=model,
+                               global_offset=global_offset, global_n=global_n)
+
+    def knn(self, queries: torch.Tensor, k: int):
+        from .index import merge_topk
+        return sharded_knn(queries, k, self.index.knn, merge_topk, self.group)

@@ -187,7 +187,7 @@ def test_bsf_init_prunes_without_changing_results():
     bsf = (d0[:, 0] ** 2) * 1.001
     d1, i1, s1 = ix.knn(q, 1, bsf_init=bsf.contiguous(), stats=True)
     assert torch.equal(i0, i1)
-    tight = (d0[:, 0] ** 2) * 0.5          # bound below the true NN: nothing may be returned
+    tight = (d0[:, 0] ** 2) * 0.5          # bound below the true NN: nothing within it exists
     d2, i2 = ix.knn(q, 1, bsf_init=tight.contiguous())
     assert bool((i2 == -1).all()) and bool(torch.isinf(d2).all())
 
