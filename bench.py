@@ -233,12 +233,12 @@ def main():
             torch.cuda.synchronize()
             barrier()
             times.append(s0.elapsed_time(s1))
+        launches = S.sofa_launch_count() - launches0
         # keep sampling clocks for a short sustained run of the same step (no timing taken)
         t_end = time.time() + 1.0
         while time.time() < t_end:
             knn(q)
         torch.cuda.synchronize()
-    launches = S.sofa_launch_count() - launches0
     tot_ms = max_over_ranks(sum(times))
     ms_per_step = tot_ms / a.steps
     value = w.n_queries * a.steps / (tot_ms / 1e3)

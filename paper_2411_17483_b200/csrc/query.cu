@@ -96,7 +96,7 @@ __device__ __forceinline__ void warp_append(bool pass, unsigned long long key, u
 }
 
 struct QShared {
-  int qi, cnt, ncand, tkn, b0;
+  int qi, cnt, ncand, tkn, b0, take, rem;
   float bsf, bsf_init, thr;
   unsigned long long st[6];  // blocks_survived, words_scanned, candidates, refined, abandoned, -
 };
@@ -143,14 +143,14 @@ __device__ __forceinline__ float ed_warp(const float* __restrict__ row, float2 s
   return total;
 }
 
-// word LB (d_SFA^2 from the T table) with chunked early abandoning: Alg. 3
+// word LB (d_SFA^2 from the T table) with chunked early abandoning: Alg. 3.  The word's
+// 16-byte chunks were loaded beforehand (all loads of a batch are in flight together).
 template <int LT>
-__device__ __forceinline__ float word_lb(const uint8_t* __restrict__ wp, const float* __restrict__ sT, float thr) {
+__device__ __forceinline__ float word_lb(const uint4 (&w)[LT / 16], const float* __restrict__ sT, float thr) {
   float lb = 0.f;
 #pragma unroll
   for (int c = 0; c < LT / 16; ++c) {
-    const uint4 w = ld_stream_u4(wp + 16 * c);
-    const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+    const uint32_t wv[4] = {w[c].x, w[c].y, w[c].z, w[c].w};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {  // two chunks of 8 positions per 16 bytes
 #pragma unroll
@@ -247,20 +247,32 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
         S.st[0] += surv;
       }
       unsigned long long scanned = 0;
-      for (int w = tid; w < CAP_C; w += kThreads) {
+      constexpr int WPT = CAP_C / kThreads;  // words per thread per batch
+      int64_t pos[WPT];
+      bool valid[WPT];
+      uint4 wr[WPT][LT / 16];
+#pragma unroll
+      for (int t = 0; t < WPT; ++t) {  // issue every load of the batch first
+        const int w = tid + t * kThreads;
         const int u = w / span, m = w % span;
         const int e = e0 + u;
-        bool valid = e < cnt && u < G;
-        int64_t pos = 0;
-        if (valid) {
+        valid[t] = e < cnt && u < G;
+        pos[t] = 0;
+        if (valid[t]) {
           const unsigned long long ent = list[e];
-          pos = (int64_t)(uint32_t)ent * B + (int64_t)sub * CAP_C + m;
-          valid = lb_of(ent) <= thr && pos < A.n;
+          pos[t] = (int64_t)(uint32_t)ent * B + (int64_t)sub * CAP_C + m;
+          valid[t] = lb_of(ent) <= thr && pos[t] < A.n;
         }
+#pragma unroll
+        for (int c = 0; c < LT / 16; ++c)
+          wr[t][c] = valid[t] ? ld_stream_u4(A.words + pos[t] * A.WS + 16 * c) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int t = 0; t < WPT; ++t) {
         float lb = INFINITY;
-        if (valid) lb = word_lb<LT>(A.words + pos * A.WS, s_T, thr);
-        scanned += valid;
-        warp_append(valid && lb <= thr, pack(lb, (uint32_t)pos), s_cand, &S.ncand);
+        if (valid[t]) lb = word_lb<LT>(wr[t], s_T, thr);
+        scanned += valid[t];
+        warp_append(valid[t] && lb <= thr, pack(lb, (uint32_t)pos[t]), s_cand, &S.ncand);
       }
       if (scanned) atomicAdd(&S.st[1], scanned);
       __syncthreads();
@@ -294,7 +306,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int len = A.len, nf4 = len >> 2, l = A.l, a = A.a;
-  unsigned long long* gl = A.gscratch + (int64_t)blockIdx.x * A.nb;
+  unsigned long long* gl = A.gscratch + (int64_t)blockIdx.x * 2 * A.nb;
+  unsigned long long* gl2 = gl + A.nb;
 
   for (;;) {
     if (tid == 0) S.qi = atomicAdd(A.qcounter, 1);
@@ -416,18 +429,63 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
       }
     }
     __syncthreads();
-    const int cnt = S.cnt;
-    const unsigned long long* list = gl;
-    bool sorted = false;
-    if (cnt <= CAP_B) {  // Tlo/Thi are dead now: the union holds the block list
-      for (int i = tid; i < cnt; i += kThreads) s_blist[i] = gl[i];
-      __syncthreads();
-      bitonic_sort_u64(s_blist, cnt);
-      list = s_blist;
-      sorted = true;
+    // ---------------------------------------------------------------- a6 -> a7/a8: LB-ordered rounds
+    // MESSI processes leaves in ascending LB from priority queues.  Here: if the
+    // surviving blocks fit in shared memory, bitonic-sort them all; otherwise take the ~CAP_B/2
+    // lowest-LB blocks (threshold tau from a sorted strided sample of 256 entries), sort and
+    // process those, re-filter the rest against the tightened BSF, and repeat.
+    {
+      int cnt = S.cnt;
+      unsigned long long* cur = gl;
+      unsigned long long* nxt = gl2;
+      while (cnt > 0) {
+        if (cnt <= CAP_B) {
+          for (int i = tid; i < cnt; i += kThreads) s_blist[i] = cur[i];
+          __syncthreads();
+          bitonic_sort_u64(s_blist, cnt);
+          scan_blocks<LT, NF>(A, S, s_blist, cnt, true, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+          break;
+        }
+        s_cand[tid] = cur[((int64_t)tid * cnt) / kThreads];
+        if (tid == 0) {
+          S.take = 0;
+          S.rem = 0;
+        }
+        __syncthreads();
+        bitonic_sort_u64(s_cand, kThreads);
+        int r = (int)(((int64_t)kThreads * (CAP_B / 2)) / cnt);
+        r = r < 0 ? 0 : (r > kThreads - 1 ? kThreads - 1 : r);
+        const float tau = lb_of(s_cand[r]);
+        const float thr = S.thr;
+        for (int ee = warp * 32; ee < cnt; ee += kThreads) {
+          const int e = ee + lane;
+          const unsigned long long ent = e < cnt ? cur[e] : ~0ull;
+          const float lbe = lb_of(ent);
+          const bool keep = e < cnt && lbe <= thr;
+          const bool take = keep && lbe <= tau;
+          const unsigned m = __ballot_sync(FULL, take);
+          int base = 0;
+          if (m) {
+            const int leader = __ffs(m) - 1;
+            if (lane == leader) base = atomicAdd(&S.take, __popc(m));
+            base = __shfl_sync(FULL, base, leader);
+          }
+          const int slot = base + __popc(m & ((1u << lane) - 1u));
+          const bool got = take && slot < CAP_B;
+          if (got) s_blist[slot] = ent;
+          warp_append(keep && !got, ent, nxt, &S.rem);
+        }
+        __syncthreads();
+        const int ntake = S.take < CAP_B ? S.take : CAP_B;
+        const int nrem = S.rem;
+        bitonic_sort_u64(s_blist, ntake);
+        scan_blocks<LT, NF>(A, S, s_blist, ntake, true, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+        unsigned long long* t = cur;
+        cur = nxt;
+        nxt = t;
+        cnt = nrem;
+      }
     }
-    // ---------------------------------------------------------------- a7 + a8
-    scan_blocks<LT, NF>(A, S, list, cnt, sorted, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
     // ---------------------------------------------------------------- output
     for (int r = tid; r < A.k; r += kThreads) {
       const bool ok = r < S.tkn;
@@ -457,7 +515,7 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
   if (per_sm < 1) per_sm = 1;
   int grid = sms * per_sm;
   if (grid > A.q) grid = A.q;
-  const int64_t need = (int64_t)grid * (ix->nb > 0 ? ix->nb : 1);
+  const int64_t need = (int64_t)grid * 2 * (ix->nb > 0 ? ix->nb : 1);
   if (ix->gscratch_ctas < need) {
     if (ix->gscratch) cudaFree(ix->gscratch);
     ix->gscratch = nullptr;

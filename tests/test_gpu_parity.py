@@ -216,8 +216,13 @@ def test_edge_cases_small_and_degenerate():
 
 def test_single_series_and_padding_and_short_len():
     rng = np.random.default_rng(6)
+    from paper_2411_17483_b200.sofa import SofaError
     x = torch.from_numpy(rng.normal(size=(1, 8)).astype(np.float32)).cuda()
-    ix = SofaIndex(x, l=3, alphabet=2, sample_size=2, binning="equi-width")
+    with pytest.raises(SofaError, match="at least 2 rows"):      # variance needs >= 2 sample rows
+        SofaIndex(x, l=3, alphabet=2, sample_size=2, binning="equi-width")
+    other = torch.from_numpy(rng.normal(size=(64, 8)).astype(np.float32)).cuda()
+    m1 = SofaIndex(other, l=3, alphabet=2, sample_size=64, binning="equi-width").raw_model
+    ix = SofaIndex(x, l=3, alphabet=2, model=m1)                # a single series with a given model
     d, i = ix.knn(x, 1)
     assert i.item() == 0 and d.item() == 0.0
     x4 = torch.from_numpy(rng.normal(size=(500, 4)).astype(np.float32)).cuda()
