@@ -98,7 +98,7 @@ __device__ __forceinline__ void warp_append(bool pass, unsigned long long key, u
 struct QShared {
   int qi, cnt, ncand, tkn, b0, take, rem;
   float bsf, bsf_init, thr;
-  unsigned long long st[6];  // blocks_survived, words_scanned, candidates, refined, abandoned, -
+  unsigned int st[6];  // per query: blocks_survived, words_scanned, candidates, refined, abandoned, -
 };
 
 // exact squared z-ED with early abandoning (a8): one warp, float4 loads, chunk = 2 float4 / lane
@@ -192,8 +192,8 @@ __device__ void refine_candidates(const QArgs& A, QShared& S, unsigned long long
     if (lane == 0) {
       s_wd[warp] = (did && !ab) ? d2 : INFINITY;
       s_wi[warp] = (did && !ab) ? oidx : -1;
-      if (did) atomicAdd(&S.st[3], 1ull);
-      if (ab) atomicAdd(&S.st[4], 1ull);
+      if (did) atomicAdd(&S.st[3], 1u);
+      if (ab) atomicAdd(&S.st[4], 1u);
     }
     __syncthreads();
     if (tid == 0) {
@@ -242,11 +242,11 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
       const float thr = S.thr;
       if (sorted && lb_of(list[e0]) > thr) return;  // every later block has a larger LB
       if (tid == 0 && sub == 0) {
-        unsigned long long surv = 0;
+        unsigned int surv = 0;
         for (int u = 0; u < G && e0 + u < cnt; ++u) surv += lb_of(list[e0 + u]) <= thr;
         S.st[0] += surv;
       }
-      unsigned long long scanned = 0;
+      unsigned int scanned = 0;
       constexpr int WPT = CAP_C / kThreads;  // words per thread per batch
       int64_t pos[WPT];
       bool valid[WPT];
@@ -274,7 +274,8 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
         scanned += valid[t];
         warp_append(valid[t] && lb <= thr, pack(lb, (uint32_t)pos[t]), s_cand, &S.ncand);
       }
-      if (scanned) atomicAdd(&S.st[1], scanned);
+      scanned = __reduce_add_sync(FULL, scanned);
+      if ((tid & 31) == 0 && scanned) atomicAdd(&S.st[1], scanned);
       __syncthreads();
       if (tid == 0) S.st[2] += S.ncand;
       refine_candidates<LT, NF>(A, S, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
     if (tid == 0 && A.dstats) {
       atomicAdd(&A.dstats[0], 1ull);
       atomicAdd(&A.dstats[1], (unsigned long long)A.nb);
-      for (int i = 0; i < 5; ++i) atomicAdd(&A.dstats[2 + i], S.st[i]);
+      for (int i = 0; i < 5; ++i) atomicAdd(&A.dstats[2 + i], (unsigned long long)S.st[i]);
     }
     __syncthreads();
   }
