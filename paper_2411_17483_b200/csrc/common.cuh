@@ -140,6 +140,8 @@ struct sofa_index {
   int32_t* perm = nullptr;        // n: sorted position -> local row
   uint8_t* env = nullptr;         // nb x 2 x WS
   uint64_t* bkey = nullptr;       // nb first keys
+  int nlev = 1;                   // envelope tree levels (level 0 = blocks, fan-out 16)
+  int64_t lvl_off[8] = {}, lvl_cnt[8] = {};
   float* basis32 = nullptr;
   double* basis64 = nullptr;
   float* edges32 = nullptr;
@@ -164,6 +166,7 @@ int launch_transform(const float* X, int64_t N, const DevModel& dm, uint8_t* wor
                      double* vals, uint8_t* words_l, cudaStream_t st);
 int launch_envelopes(const uint8_t* words, int64_t n, int B, int WS, const uint64_t* skeys, uint8_t* env,
                      uint64_t* bkey, cudaStream_t st);
+int launch_env_up(const uint8_t* child, int64_t nchild, int WS, uint8_t* parent, cudaStream_t st);
 int launch_gather(const uint8_t* words, const float2* stats, const int32_t* perm, int64_t n, int WS,
                   uint8_t* words_out, float2* stats_out, cudaStream_t st);
 int learn_model_dev(const float* sample, int64_t S, int len, int l, int a, int binning, int cand_limit,

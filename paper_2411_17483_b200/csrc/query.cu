@@ -30,6 +30,7 @@ namespace sofa {
 constexpr int CAP_B = 2048;  // surviving blocks sorted in shared memory
 constexpr int CAP_C = 1024;  // words per scan batch = candidate buffer capacity
 constexpr int KMAX = SOFA_MAX_K;
+constexpr int kFan = 16;  // envelope tree fan-out
 
 struct QArgs {
   const float* series;
@@ -49,6 +50,8 @@ struct QArgs {
   int64_t* oi;
   int64_t goff;
   unsigned long long* gscratch;
+  int nlev;
+  int64_t lvl_off[8], lvl_cnt[8];
   int* qcounter;
   unsigned long long* dstats;
   float weights[SOFA_MAX_L];
@@ -227,7 +230,9 @@ __device__ void refine_candidates(const QArgs& A, QShared& S, unsigned long long
   __syncthreads();
 }
 
-// scan the words of the listed blocks (a7) and refine (a8), batch by batch
+// scan the words of the listed blocks (a7) and refine (a8), batch by batch.  The words of batch
+// i+1 are loaded into registers before batch i's candidates are appended and refined, so their
+// HBM latency overlaps the refine (software pipelining over the batch loop).
 template <int LT, int NF>
 __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long* list, int cnt, bool sorted,
                             const float* s_T, unsigned long long* s_cand, float* s_tkd, int* s_tki, float* s_wd,
@@ -237,48 +242,119 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
   const int G = B <= CAP_C ? CAP_C / B : 1;    // blocks per batch
   const int SUB = B <= CAP_C ? 1 : B / CAP_C;  // batches per block
   const int span = B <= CAP_C ? B : CAP_C;
-  for (int e0 = 0; e0 < cnt; e0 += G) {
-    for (int sub = 0; sub < SUB; ++sub) {
-      const float thr = S.thr;
-      if (sorted && lb_of(list[e0]) > thr) return;  // every later block has a larger LB
-      if (tid == 0 && sub == 0) {
-        unsigned int surv = 0;
-        for (int u = 0; u < G && e0 + u < cnt; ++u) surv += lb_of(list[e0 + u]) <= thr;
-        S.st[0] += surv;
-      }
-      unsigned int scanned = 0;
-      constexpr int WPT = CAP_C / kThreads;  // words per thread per batch
-      int64_t pos[WPT];
-      bool valid[WPT];
-      uint4 wr[WPT][LT / 16];
+  const int nbatch = ((cnt + G - 1) / G) * SUB;
+  if (nbatch == 0) return;
+  constexpr int WPT = CAP_C / kThreads;  // words per thread per batch
+  constexpr int NC = LT / 16;
+  int64_t pos[WPT];
+  bool valid[WPT];
+  uint4 wr[WPT][NC];
+  auto issue = [&](int bi, float thr) {
+    const int e0 = (bi / SUB) * G, sub = bi % SUB;
 #pragma unroll
-      for (int t = 0; t < WPT; ++t) {  // issue every load of the batch first
-        const int w = tid + t * kThreads;
-        const int u = w / span, m = w % span;
-        const int e = e0 + u;
-        valid[t] = e < cnt && u < G;
-        pos[t] = 0;
-        if (valid[t]) {
-          const unsigned long long ent = list[e];
-          pos[t] = (int64_t)(uint32_t)ent * B + (int64_t)sub * CAP_C + m;
-          valid[t] = lb_of(ent) <= thr && pos[t] < A.n;
-        }
-#pragma unroll
-        for (int c = 0; c < LT / 16; ++c)
-          wr[t][c] = valid[t] ? ld_stream_u4(A.words + pos[t] * A.WS + 16 * c) : make_uint4(0u, 0u, 0u, 0u);
+    for (int t = 0; t < WPT; ++t) {
+      const int w = tid + t * kThreads;
+      const int u = w / span, m = w % span;
+      const int e = e0 + u;
+      valid[t] = bi < nbatch && e < cnt && u < G;
+      pos[t] = 0;
+      if (valid[t]) {
+        const unsigned long long ent = list[e];
+        pos[t] = (int64_t)(uint32_t)ent * B + (int64_t)sub * CAP_C + m;
+        valid[t] = lb_of(ent) <= thr && pos[t] < A.n;
       }
 #pragma unroll
-      for (int t = 0; t < WPT; ++t) {
-        float lb = INFINITY;
-        if (valid[t]) lb = word_lb<LT>(wr[t], s_T, thr);
-        scanned += valid[t];
-        warp_append(valid[t] && lb <= thr, pack(lb, (uint32_t)pos[t]), s_cand, &S.ncand);
+      for (int c = 0; c < NC; ++c)
+        wr[t][c] = valid[t] ? ld_stream_u4(A.words + pos[t] * A.WS + 16 * c) : make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+  issue(0, S.thr);
+  for (int bi = 0; bi < nbatch; ++bi) {
+    const float thr = S.thr;
+    const int e0 = (bi / SUB) * G, sub = bi % SUB;
+    if (sorted && lb_of(list[e0]) > thr) return;  // every later block has a larger LB
+    if (tid == 0 && sub == 0) {
+      unsigned int surv = 0;
+      for (int u = 0; u < G && e0 + u < cnt; ++u) surv += lb_of(list[e0 + u]) <= thr;
+      S.st[0] += surv;
+    }
+    float lbs[WPT];
+    bool vcur[WPT];
+    int64_t pcur[WPT];
+    unsigned int scanned = 0;
+#pragma unroll
+    for (int t = 0; t < WPT; ++t) {
+      vcur[t] = valid[t];
+      pcur[t] = pos[t];
+      lbs[t] = valid[t] ? word_lb<LT>(wr[t], s_T, thr) : INFINITY;
+      scanned += valid[t];
+    }
+    issue(bi + 1, thr);  // next batch's loads fly during this batch's append + refine
+#pragma unroll
+    for (int t = 0; t < WPT; ++t)
+      warp_append(vcur[t] && lbs[t] <= thr, pack(lbs[t], (uint32_t)pcur[t]), s_cand, &S.ncand);
+    scanned = __reduce_add_sync(FULL, scanned);
+    if ((tid & 31) == 0 && scanned) atomicAdd(&S.st[1], scanned);
+    __syncthreads();
+    if (tid == 0) S.st[2] += S.ncand;
+    refine_candidates<LT, NF>(A, S, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+  }
+}
+
+// envelope LB of a node (leaf LB): sum_j Tlo[j][min_j] + Thi[j][max_j]
+template <int LT>
+__device__ __forceinline__ float env_lb(const uint4 (&mn)[LT / 16], const uint4 (&mx)[LT / 16], const float* sTlo,
+                                        const float* sThi) {
+  float lb = 0.f;
+#pragma unroll
+  for (int c = 0; c < LT / 16; ++c) {
+    const uint32_t vn[4] = {mn[c].x, mn[c].y, mn[c].z, mn[c].w}, vx[4] = {mx[c].x, mx[c].y, mx[c].z, mx[c].w};
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      const int j = c * 16 + jj;
+      lb += sTlo[j * 256 + ((vn[jj >> 2] >> (8 * (jj & 3))) & 0xffu)];
+      lb += sThi[j * 256 + ((vx[jj >> 2] >> (8 * (jj & 3))) & 0xffu)];
+    }
+  }
+  return lb;
+}
+
+// One level of the envelope tree: either every node of the level (parents == nullptr) or the
+// F children of each listed parent whose LB is still <= thr.  Survivors (LB, node) -> out.
+template <int LT>
+__device__ void env_level(const QArgs& A, int L, const unsigned long long* parents, int nparents, int64_t b0,
+                          float thr, const float* sTlo, const float* sThi, unsigned long long* out, int* counter) {
+  constexpr int NC = LT / 16, U = 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int WS = A.WS;
+  const uint8_t* base = A.env + A.lvl_off[L] * 2 * WS;
+  const int64_t ncnt = A.lvl_cnt[L];
+  const int64_t total = parents ? (int64_t)nparents * kFan : ncnt;
+  for (int64_t ii = (int64_t)warp * 32 * U; ii < total; ii += (int64_t)kThreads * U) {
+    int64_t node[U];
+    bool ok[U];
+    uint4 mn[U][NC], mx[U][NC];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t idx = ii + u * 32 + lane;
+      ok[u] = idx < total;
+      node[u] = idx;
+      if (ok[u] && parents) {
+        const unsigned long long pe = parents[idx / kFan];
+        node[u] = (int64_t)(uint32_t)pe * kFan + idx % kFan;
+        ok[u] = lb_of(pe) <= thr && node[u] < ncnt;
       }
-      scanned = __reduce_add_sync(FULL, scanned);
-      if ((tid & 31) == 0 && scanned) atomicAdd(&S.st[1], scanned);
-      __syncthreads();
-      if (tid == 0) S.st[2] += S.ncand;
-      refine_candidates<LT, NF>(A, S, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+      ok[u] = ok[u] && !(L == 0 && node[u] == b0);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        mn[u][c] = ok[u] ? ld_stream_u4(base + node[u] * 2 * WS + 16 * c) : make_uint4(0u, 0u, 0u, 0u);
+        mx[u][c] = ok[u] ? ld_stream_u4(base + node[u] * 2 * WS + WS + 16 * c) : make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float lb = ok[u] ? env_lb<LT>(mn[u], mx[u], sTlo, sThi) : INFINITY;
+      warp_append(ok[u] && lb <= thr, pack(lb, (uint32_t)node[u]), out, counter);
     }
   }
 }
@@ -403,33 +479,31 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
     if (tid == 0) s_seed = pack(0.f, (uint32_t)b0);
     __syncthreads();
     scan_blocks<LT, NF>(A, S, &s_seed, A.nb > 0 ? 1 : 0, true, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
-    // ---------------------------------------------------------------- a6: envelope LB scan
+    // ---------------------------------------------------------------- a6: envelope tree descent
+    // top level: every node; lower levels: the kFan children of each surviving parent
+    // (the MESSI-style tree over sorted SFA-word blocks, P:159-166 / P:171-173)
     {
       const float thr = S.thr;
-      const int WS = A.WS;
-      for (int64_t bb = (int64_t)warp * 32; bb < A.nb; bb += kThreads) {
-        const int64_t b = bb + lane;
-        const bool valid = b < A.nb && b != b0;
-        float lb = INFINITY;
-        if (valid) {
-          const uint8_t* ev = A.env + b * 2 * WS;
-          lb = 0.f;
-#pragma unroll
-          for (int c = 0; c < LT / 16; ++c) {
-            const uint4 mn = ld_stream_u4(ev + 16 * c), mx = ld_stream_u4(ev + WS + 16 * c);
-            const uint32_t vn[4] = {mn.x, mn.y, mn.z, mn.w}, vx[4] = {mx.x, mx.y, mx.z, mx.w};
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) {
-              const int j = c * 16 + jj;
-              lb += s_Tlo[j * 256 + ((vn[jj >> 2] >> (8 * (jj & 3))) & 0xffu)];
-              lb += s_Thi[j * 256 + ((vx[jj >> 2] >> (8 * (jj & 3))) & 0xffu)];
-            }
-          }
-        }
-        warp_append(valid && lb <= thr, pack(lb, (uint32_t)b), gl, &S.cnt);
+      unsigned long long* cur = gl;
+      unsigned long long* nxt = gl2;
+      env_level<LT>(A, A.nlev - 1, nullptr, 0, b0, thr, s_Tlo, s_Thi, cur, &S.cnt);
+      for (int L = A.nlev - 2; L >= 0; --L) {
+        __syncthreads();
+        const int np = S.cnt;
+        if (tid == 0) S.rem = 0;
+        __syncthreads();
+        env_level<LT>(A, L, cur, np, b0, S.thr, s_Tlo, s_Thi, nxt, &S.rem);
+        __syncthreads();
+        if (tid == 0) S.cnt = S.rem;
+        unsigned long long* t = cur;
+        cur = nxt;
+        nxt = t;
+      }
+      if (cur != gl) {  // the rounds below start from gl
+        __syncthreads();
+        for (int i = tid; i < S.cnt; i += kThreads) gl[i] = cur[i];
       }
     }
-    __syncthreads();
     // ---------------------------------------------------------------- a6 -> a7/a8: LB-ordered rounds
     // MESSI processes leaves in ascending LB from priority queues.  Here: if the
     // surviving blocks fit in shared memory, bitonic-sort them all; otherwise take the ~CAP_B/2
@@ -546,6 +620,11 @@ int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_
   A.perm = ix->perm;
   A.env = ix->env;
   A.bkey = ix->bkey;
+  A.nlev = ix->nlev;
+  for (int L = 0; L < 8; ++L) {
+    A.lvl_off[L] = ix->lvl_off[L];
+    A.lvl_cnt[L] = ix->lvl_cnt[L];
+  }
   A.edges64 = ix->edges64;
   A.basis64 = ix->basis64;
   A.Q = Q;

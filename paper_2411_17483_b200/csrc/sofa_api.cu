@@ -258,7 +258,17 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
   BCK(cudaMalloc(&ix->perm, (size_t)n * 4));
   BCK(cudaMalloc(&ix->words, (size_t)n * WS));
   BCK(cudaMalloc(&ix->stats, (size_t)n * 8));
-  BCK(cudaMalloc(&ix->env, (size_t)ix->nb * 2 * WS));
+  // envelope tree: level 0 = blocks, each level up groups 16 nodes, until <= 2048 nodes remain
+  ix->nlev = 1;
+  ix->lvl_cnt[0] = ix->nb;
+  ix->lvl_off[0] = 0;
+  while (ix->lvl_cnt[ix->nlev - 1] > 2048 && ix->nlev < 8) {
+    ix->lvl_off[ix->nlev] = ix->lvl_off[ix->nlev - 1] + ix->lvl_cnt[ix->nlev - 1];
+    ix->lvl_cnt[ix->nlev] = (ix->lvl_cnt[ix->nlev - 1] + 15) / 16;
+    ix->nlev++;
+  }
+  const int64_t env_nodes = ix->lvl_off[ix->nlev - 1] + ix->lvl_cnt[ix->nlev - 1];
+  BCK(cudaMalloc(&ix->env, (size_t)env_nodes * 2 * WS));
   BCK(cudaMalloc(&ix->bkey, (size_t)ix->nb * 8));
   if ((rc = launch_transform(series_dev, n, ix->dm, words_u, stats_u, keys_u, nullptr, nullptr, st))) {
     freeall();
@@ -277,6 +287,12 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
     freeall();
     return bail(rc);
   }
+  for (int L = 1; L < ix->nlev; ++L)
+    if ((rc = launch_env_up(ix->env + ix->lvl_off[L - 1] * 2 * WS, ix->lvl_cnt[L - 1], WS,
+                            ix->env + ix->lvl_off[L] * 2 * WS, st))) {
+      freeall();
+      return bail(rc);
+    }
   BCK(cudaStreamSynchronize(st));
 #undef BCK
   freeall();

@@ -278,6 +278,37 @@ __global__ void k_envelopes(const uint8_t* __restrict__ words, int64_t n, int B,
   }
 }
 
+// a4: one level up the envelope tree: a parent's envelope is the min of its 16 children's mins and
+// the max of their maxes (so parent LB <= child LB <= member LB).
+__global__ void k_env_up(const uint8_t* __restrict__ child, int64_t nchild, int WS, uint8_t* __restrict__ parent) {
+  const int parts = WS >> 4;
+  const int64_t npar = (nchild + 15) / 16;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npar * parts;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / parts;
+    const int c = (int)(i % parts);
+    uint4 mn = make_uint4(~0u, ~0u, ~0u, ~0u), mx = make_uint4(0u, 0u, 0u, 0u);
+    for (int64_t ch = p * 16; ch < p * 16 + 16 && ch < nchild; ++ch) {
+      const uint4 a = *reinterpret_cast<const uint4*>(child + ch * 2 * WS + c * 16);
+      const uint4 b = *reinterpret_cast<const uint4*>(child + ch * 2 * WS + WS + c * 16);
+      mn.x = __vminu4(mn.x, a.x); mn.y = __vminu4(mn.y, a.y); mn.z = __vminu4(mn.z, a.z); mn.w = __vminu4(mn.w, a.w);
+      mx.x = __vmaxu4(mx.x, b.x); mx.y = __vmaxu4(mx.y, b.y); mx.z = __vmaxu4(mx.z, b.z); mx.w = __vmaxu4(mx.w, b.w);
+    }
+    *reinterpret_cast<uint4*>(parent + p * 2 * WS + c * 16) = mn;
+    *reinterpret_cast<uint4*>(parent + p * 2 * WS + WS + c * 16) = mx;
+  }
+}
+
+int launch_env_up(const uint8_t* child, int64_t nchild, int WS, uint8_t* parent, cudaStream_t st) {
+  const int64_t tot = (nchild + 15) / 16 * (WS >> 4);
+  int grid = (int)((tot + kThreads - 1) / kThreads);
+  if (grid > 148 * 16) grid = 148 * 16;
+  if (grid < 1) grid = 1;
+  k_env_up<<<grid, kThreads, 0, st>>>(child, nchild, WS, parent);
+  SOFA_LAUNCHED();
+  return SOFA_OK;
+}
+
 int launch_envelopes(const uint8_t* words, int64_t n, int B, int WS, const uint64_t* skeys, uint8_t* env,
                      uint64_t* bkey, cudaStream_t st) {
   const int64_t nb = (n + B - 1) / B;
