@@ -503,6 +503,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
         __syncthreads();
         for (int i = tid; i < S.cnt; i += kThreads) gl[i] = cur[i];
       }
+      __syncthreads();  // S.cnt and gl are final for every thread
     }
     // ---------------------------------------------------------------- a6 -> a7/a8: LB-ordered rounds
     // MESSI processes leaves in ascending LB from priority queues.  Here: if the
