@@ -246,7 +246,9 @@ def main():
     # ---------------------------------------------------------------- roofline of the query kernel
     hbm, peak_kind = peaks()
     l_b, n_b = w.l, 4 * w.length
-    alg_bytes = (st["blocks_total"] * 2 * l_b + st["words_scanned"] * l_b + st["refined"] * n_b
+    # algorithmic bytes (SURVEY 8(d) unit costs): envelope nodes the tree descent evaluated (2l B each),
+    # words of surviving blocks (l B each), refined rows (4n B each), the query rows (4n B each)
+    alg_bytes = (st["env_nodes"] * 2 * l_b + st["words_scanned"] * l_b + st["refined"] * n_b
                  + st["queries"] * n_b)
     kern_ms = statistics.median(times)   # at N=1 the step is the query kernel (+ a 4-byte memset)
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
@@ -310,6 +312,7 @@ def main():
                       "block": 1.0 - st["blocks_survived"] / max(1, st["blocks_total"]),
                       "refined_per_query": st["refined"] / st["queries"],
                       "words_scanned_per_query": st["words_scanned"] / st["queries"]},
+            "knn_stats": st,
             "build": {"ms": build_ms, "gb_per_s_series_read": (hi - lo) * w.length * 4 / (build_ms / 1e3) / 1e9},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,

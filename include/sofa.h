@@ -93,6 +93,12 @@ typedef struct {
   int64_t candidates;       /* words with LB <= threshold */
   int64_t refined;          /* exact distance computations started */
   int64_t abandoned;        /* of those, early-abandoned */
+  int64_t env_nodes;        /* envelope-tree nodes whose LB was evaluated (all levels) */
+  int64_t list_blocks;      /* leaf blocks left after the tree descent (before BSF re-checks) */
+  int64_t rounds;           /* LB-ordered selection rounds */
+  int64_t batches;          /* word-scan batches */
+  int64_t waves;            /* refine waves (8 candidates each) */
+  int64_t phase_cycles[4];  /* SM cycles summed over queries: prep+tables, seed, tree, scan+refine */
 } sofa_knn_stats;
 
 /* Fill *out with defaults (sample_ratio 0.01, block_size 256, equi-depth, everything else 0). */

@@ -101,7 +101,9 @@ __device__ __forceinline__ void warp_append(bool pass, unsigned long long key, u
 struct QShared {
   int qi, cnt, ncand, tkn, b0, take, rem;
   float bsf, bsf_init, thr;
-  unsigned int st[6];  // per query: blocks_survived, words_scanned, candidates, refined, abandoned, -
+  // per query: 0 blocks_survived, 1 words_scanned, 2 candidates, 3 refined, 4 abandoned, 5 env_nodes,
+  // 6 list_blocks, 7 rounds, 8 batches, 9 waves
+  unsigned int st[10];
 };
 
 // exact squared z-ED with early abandoning (a8): one warp, float4 loads, chunk = 2 float4 / lane
@@ -192,6 +194,7 @@ __device__ void refine_candidates(const QArgs& A, QShared& S, unsigned long long
         d2 = ed_warp<NF>(A.series + (int64_t)oidx * A.len, st, s_qh4, nf4, bsf, ab);
       }
     }
+    if (tid == 0) S.st[9] += 1;
     if (lane == 0) {
       s_wd[warp] = (did && !ab) ? d2 : INFINITY;
       s_wi[warp] = (did && !ab) ? oidx : -1;
@@ -273,6 +276,7 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
     const float thr = S.thr;
     const int e0 = (bi / SUB) * G, sub = bi % SUB;
     if (sorted && lb_of(list[e0]) > thr) return;  // every later block has a larger LB
+    if (tid == 0) S.st[8] += 1;
     if (tid == 0 && sub == 0) {
       unsigned int surv = 0;
       for (int u = 0; u < G && e0 + u < cnt; ++u) surv += lb_of(list[e0 + u]) <= thr;
@@ -323,7 +327,8 @@ __device__ __forceinline__ float env_lb(const uint4 (&mn)[LT / 16], const uint4 
 // F children of each listed parent whose LB is still <= thr.  Survivors (LB, node) -> out.
 template <int LT>
 __device__ void env_level(const QArgs& A, int L, const unsigned long long* parents, int nparents, int64_t b0,
-                          float thr, const float* sTlo, const float* sThi, unsigned long long* out, int* counter) {
+                          float thr, const float* sTlo, const float* sThi, unsigned long long* out, int* counter,
+                          unsigned int& stat_env) {
   constexpr int NC = LT / 16, U = 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int WS = A.WS;
@@ -351,11 +356,15 @@ __device__ void env_level(const QArgs& A, int L, const unsigned long long* paren
         mx[u][c] = ok[u] ? ld_stream_u4(base + node[u] * 2 * WS + WS + 16 * c) : make_uint4(0u, 0u, 0u, 0u);
       }
     }
+    unsigned int nev = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const float lb = ok[u] ? env_lb<LT>(mn[u], mx[u], sTlo, sThi) : INFINITY;
+      nev += ok[u];
       warp_append(ok[u] && lb <= thr, pack(lb, (uint32_t)node[u]), out, counter);
     }
+    nev = __reduce_add_sync(FULL, nev);
+    if (lane == 0 && nev) atomicAdd(&stat_env, nev);
   }
 }
 
@@ -391,6 +400,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
     __syncthreads();
     const int qi = S.qi;
     if (qi >= A.q) break;
+    long long t_phase[5];
+    t_phase[0] = clock64();
     // ---------------------------------------------------------------- a5: z-norm + projection
     if (warp == 0) {
       const float4* q4 = reinterpret_cast<const float4*>(A.Q + (int64_t)qi * len);
@@ -424,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
         S.cnt = 0;
         S.ncand = 0;
         S.tkn = 0;
-        for (int i = 0; i < 6; ++i) S.st[i] = 0;
+        for (int i = 0; i < 10; ++i) S.st[i] = 0;
         const float bi = A.bsf_init ? A.bsf_init[qi] : INFINITY;
         S.bsf_init = bi;
         S.bsf = bi;
@@ -476,9 +487,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
       lo = nlo;
     }
     const int64_t b0 = lo;
+    t_phase[1] = clock64();
     if (tid == 0) s_seed = pack(0.f, (uint32_t)b0);
     __syncthreads();
     scan_blocks<LT, NF>(A, S, &s_seed, A.nb > 0 ? 1 : 0, true, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+    t_phase[2] = clock64();
     // ---------------------------------------------------------------- a6: envelope tree descent
     // top level: every node; lower levels: the kFan children of each surviving parent
     // (the MESSI-style tree over sorted SFA-word blocks, P:159-166 / P:171-173)
@@ -486,13 +499,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
       const float thr = S.thr;
       unsigned long long* cur = gl;
       unsigned long long* nxt = gl2;
-      env_level<LT>(A, A.nlev - 1, nullptr, 0, b0, thr, s_Tlo, s_Thi, cur, &S.cnt);
+      env_level<LT>(A, A.nlev - 1, nullptr, 0, b0, thr, s_Tlo, s_Thi, cur, &S.cnt, S.st[5]);
       for (int L = A.nlev - 2; L >= 0; --L) {
         __syncthreads();
         const int np = S.cnt;
         if (tid == 0) S.rem = 0;
         __syncthreads();
-        env_level<LT>(A, L, cur, np, b0, S.thr, s_Tlo, s_Thi, nxt, &S.rem);
+        env_level<LT>(A, L, cur, np, b0, S.thr, s_Tlo, s_Thi, nxt, &S.rem, S.st[5]);
         __syncthreads();
         if (tid == 0) S.cnt = S.rem;
         unsigned long long* t = cur;
@@ -505,6 +518,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
       }
       __syncthreads();  // S.cnt and gl are final for every thread
     }
+    t_phase[3] = clock64();
     // ---------------------------------------------------------------- a6 -> a7/a8: LB-ordered rounds
     // MESSI processes leaves in ascending LB from priority queues.  Here: if the
     // surviving blocks fit in shared memory, bitonic-sort them all; otherwise take the ~CAP_B/2
@@ -514,7 +528,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
       int cnt = S.cnt;
       unsigned long long* cur = gl;
       unsigned long long* nxt = gl2;
+      if (tid == 0) S.st[6] += cnt;
       while (cnt > 0) {
+        if (tid == 0) S.st[7] += 1;
         if (cnt <= CAP_B) {
           for (int i = tid; i < cnt; i += kThreads) s_blist[i] = cur[i];
           __syncthreads();
@@ -568,10 +584,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
       A.od[(int64_t)qi * A.k + r] = ok ? sqrtf(s_tkd[r]) : INFINITY;
       A.oi[(int64_t)qi * A.k + r] = ok ? A.goff + s_tki[r] : -1;
     }
+    t_phase[4] = clock64();
     if (tid == 0 && A.dstats) {
       atomicAdd(&A.dstats[0], 1ull);
       atomicAdd(&A.dstats[1], (unsigned long long)A.nb);
-      for (int i = 0; i < 5; ++i) atomicAdd(&A.dstats[2 + i], (unsigned long long)S.st[i]);
+      for (int i = 0; i < 10; ++i) atomicAdd(&A.dstats[2 + i], (unsigned long long)S.st[i]);
+      for (int i = 0; i < 4; ++i) atomicAdd(&A.dstats[12 + i], (unsigned long long)(t_phase[i + 1] - t_phase[i]));
     }
     __syncthreads();
   }

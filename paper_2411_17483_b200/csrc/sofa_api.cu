@@ -222,7 +222,7 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
   if ((rc = upload_model(ix->model, len, ix, st))) return bail(rc);
   const int WS = ix->WS, B = ix->B;
   ix->nb = (n + B - 1) / B;
-  if (cudaMalloc(&ix->qcounter, 64) != cudaSuccess || cudaMalloc(&ix->dstats, 16 * 8) != cudaSuccess)
+  if (cudaMalloc(&ix->qcounter, 64) != cudaSuccess || cudaMalloc(&ix->dstats, 32 * 8) != cudaSuccess)
     return bail(fail(SOFA_ENOMEM, "counters"));
   if (n == 0) {
     cudaStreamSynchronize(st);
@@ -309,7 +309,7 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
   if (k > ix->global_n) return fail(SOFA_EINVAL, "k exceeds the number of series");
   if (!queries_dev || !out_dist_dev || !out_idx_dev) return fail(SOFA_EINVAL, "NULL pointer");
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  if (stats) SOFA_CK(cudaMemsetAsync(ix->dstats, 0, 16 * 8, st));
+  if (stats) SOFA_CK(cudaMemsetAsync(ix->dstats, 0, 32 * 8, st));
   int rc;
   if (ix->n == 0)
     rc = launch_fill_pad(out_dist_dev, out_idx_dev, (int64_t)q * k, st);
@@ -317,8 +317,8 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
     rc = launch_query(ix, queries_dev, q, k, bsf_init_dev, out_dist_dev, out_idx_dev, st);
   if (rc) return rc;
   if (stats) {
-    unsigned long long h[16] = {};
-    SOFA_CK(cudaMemcpyAsync(h, ix->dstats, 16 * 8, cudaMemcpyDeviceToHost, st));
+    unsigned long long h[32] = {};
+    SOFA_CK(cudaMemcpyAsync(h, ix->dstats, 32 * 8, cudaMemcpyDeviceToHost, st));
     SOFA_CK(cudaStreamSynchronize(st));
     stats->queries = q;
     stats->blocks_total = (int64_t)h[1];
@@ -327,6 +327,12 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
     stats->candidates = (int64_t)h[4];
     stats->refined = (int64_t)h[5];
     stats->abandoned = (int64_t)h[6];
+    stats->env_nodes = (int64_t)h[7];
+    stats->list_blocks = (int64_t)h[8];
+    stats->rounds = (int64_t)h[9];
+    stats->batches = (int64_t)h[10];
+    stats->waves = (int64_t)h[11];
+    for (int i = 0; i < 4; ++i) stats->phase_cycles[i] = (int64_t)h[12 + i];
   }
   return SOFA_OK;
 }

@@ -56,10 +56,13 @@ class sofa_build_opts(C.Structure):
 
 class sofa_knn_stats(C.Structure):
     _fields_ = [(f, C.c_int64) for f in ("queries", "blocks_total", "blocks_survived", "words_scanned",
-                                         "candidates", "refined", "abandoned")]
+                                         "candidates", "refined", "abandoned", "env_nodes", "list_blocks",
+                                         "rounds", "batches", "waves")] + [("phase_cycles", C.c_int64 * 4)]
 
     def to_dict(self) -> dict:
-        return {f: int(getattr(self, f)) for f, _ in self._fields_}
+        d = {f: int(getattr(self, f)) for f, _ in self._fields_ if f != "phase_cycles"}
+        d["phase_cycles"] = dict(zip(("prep", "seed", "tree", "scan_refine"), map(int, self.phase_cycles)))
+        return d
 
 
 class sofa_index_info(C.Structure):
