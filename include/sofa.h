@@ -99,6 +99,9 @@ typedef struct {
   int64_t batches;          /* word-scan batches */
   int64_t waves;            /* refine waves (8 candidates each) */
   int64_t phase_cycles[4];  /* SM cycles summed over queries: prep+tables, seed, tree, scan+refine */
+  int64_t max_query_cycles; /* slowest query (SM cycles) */
+  int64_t max_list_blocks;  /* largest per-query leaf list */
+  int64_t max_batches;      /* most word-scan batches of one query */
 } sofa_knn_stats;
 
 /* Fill *out with defaults (sample_ratio 0.01, block_size 256, equi-depth, everything else 0). */

@@ -28,7 +28,7 @@
 namespace sofa {
 
 constexpr int CAP_B = 2048;  // surviving blocks sorted in shared memory
-constexpr int CAP_C = 1024;  // words per scan batch = candidate buffer capacity
+constexpr int CAP_C = 2048;  // words per scan batch = candidate buffer capacity
 constexpr int KMAX = SOFA_MAX_K;
 constexpr int kFan = 16;  // envelope tree fan-out
 
@@ -242,12 +242,13 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
                             int* s_wi, const float4* s_qh4) {
   const int tid = threadIdx.x;
   const int B = A.B;
-  const int G = B <= CAP_C ? CAP_C / B : 1;    // blocks per batch
-  const int SUB = B <= CAP_C ? 1 : B / CAP_C;  // batches per block
-  const int span = B <= CAP_C ? B : CAP_C;
+  constexpr int BW = LT == 16 ? CAP_C : (LT == 32 ? CAP_C / 2 : CAP_C / 4);  // words per batch
+  const int G = B <= BW ? BW / B : 1;    // blocks per batch
+  const int SUB = B <= BW ? 1 : B / BW;  // batches per block
+  const int span = B <= BW ? B : BW;
   const int nbatch = ((cnt + G - 1) / G) * SUB;
   if (nbatch == 0) return;
-  constexpr int WPT = CAP_C / kThreads;  // words per thread per batch
+  constexpr int WPT = BW / kThreads;  // words per thread per batch
   constexpr int NC = LT / 16;
   int64_t pos[WPT];
   bool valid[WPT];
@@ -263,7 +264,7 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
       pos[t] = 0;
       if (valid[t]) {
         const unsigned long long ent = list[e];
-        pos[t] = (int64_t)(uint32_t)ent * B + (int64_t)sub * CAP_C + m;
+        pos[t] = (int64_t)(uint32_t)ent * B + (int64_t)sub * BW + m;
         valid[t] = lb_of(ent) <= thr && pos[t] < A.n;
       }
 #pragma unroll
@@ -365,6 +366,41 @@ __device__ void env_level(const QArgs& A, int L, const unsigned long long* paren
     }
     nev = __reduce_add_sync(FULL, nev);
     if (lane == 0 && nev) atomicAdd(&stat_env, nev);
+  }
+}
+
+// One pass over a block list: entries with LB > thr are dropped; entries with LB <= tau go to
+// the shared-memory list `take` (up to CAP_B of them), the rest to `rem`.  4 entries per thread
+// per iteration with all loads issued first.
+__device__ void filter_list(const unsigned long long* src, int cnt, float thr, float tau, unsigned long long* take,
+                            int* ntake, unsigned long long* rem, int* nrem) {
+  constexpr int U = 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int ee = warp * 32 * U; ee < cnt; ee += kThreads * U) {
+    unsigned long long ent[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = ee + u * 32 + lane;
+      ent[u] = e < cnt ? src[e] : ~0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = ee + u * 32 + lane;
+      const float lbe = lb_of(ent[u]);
+      const bool keep = e < cnt && lbe <= thr;
+      const bool tk = keep && lbe <= tau;
+      const unsigned m = __ballot_sync(FULL, tk);
+      int base = 0;
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        if (lane == leader) base = atomicAdd(ntake, __popc(m));
+        base = __shfl_sync(FULL, base, leader);
+      }
+      const int slot = base + __popc(m & ((1u << lane) - 1u));
+      const bool got = tk && slot < CAP_B;
+      if (got) take[slot] = ent[u];
+      warp_append(keep && !got, ent[u], rem, nrem);
+    }
   }
 }
 
@@ -519,63 +555,57 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
       __syncthreads();  // S.cnt and gl are final for every thread
     }
     t_phase[3] = clock64();
-    // ---------------------------------------------------------------- a6 -> a7/a8: LB-ordered rounds
-    // MESSI processes leaves in ascending LB from priority queues.  Here: if the
-    // surviving blocks fit in shared memory, bitonic-sort them all; otherwise take the ~CAP_B/2
-    // lowest-LB blocks (threshold tau from a sorted strided sample of 256 entries), sort and
-    // process those, re-filter the rest against the tightened BSF, and repeat.
+    // ---------------------------------------------------------------- a6 -> a7/a8: LB-ordered processing
+    // MESSI processes leaves in ascending LB from priority queues and abandons a queue at the
+    // first leaf whose LB exceeds the BSF.  Here: if the surviving blocks fit in
+    // shared memory they are bitonic-sorted and scanned in ascending LB with that stop rule.
+    // Otherwise the ~CAP_B lowest-LB blocks (threshold tau from a sorted strided sample) are
+    // sorted and scanned first — that tightens the BSF to (nearly) its final value — and the rest
+    // is re-filtered against it and scanned in storage order (LB re-checked per block).
     {
-      int cnt = S.cnt;
-      unsigned long long* cur = gl;
-      unsigned long long* nxt = gl2;
+      const int cnt = S.cnt;
       if (tid == 0) S.st[6] += cnt;
-      while (cnt > 0) {
+      if (cnt <= CAP_B) {
+        for (int i = tid; i < cnt; i += kThreads) s_blist[i] = gl[i];
+        __syncthreads();
+        bitonic_sort_u64(s_blist, cnt);
+        scan_blocks<LT, NF>(A, S, s_blist, cnt, true, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+      } else {
         if (tid == 0) S.st[7] += 1;
-        if (cnt <= CAP_B) {
-          for (int i = tid; i < cnt; i += kThreads) s_blist[i] = cur[i];
-          __syncthreads();
-          bitonic_sort_u64(s_blist, cnt);
-          scan_blocks<LT, NF>(A, S, s_blist, cnt, true, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
-          break;
-        }
-        s_cand[tid] = cur[((int64_t)tid * cnt) / kThreads];
+        s_cand[tid] = gl[((int64_t)tid * cnt) / kThreads];
         if (tid == 0) {
           S.take = 0;
           S.rem = 0;
         }
         __syncthreads();
         bitonic_sort_u64(s_cand, kThreads);
-        int r = (int)(((int64_t)kThreads * (CAP_B / 2)) / cnt);
+        int r = (int)(((int64_t)kThreads * (CAP_B * 3 / 4)) / cnt);
         r = r < 0 ? 0 : (r > kThreads - 1 ? kThreads - 1 : r);
         const float tau = lb_of(s_cand[r]);
-        const float thr = S.thr;
-        for (int ee = warp * 32; ee < cnt; ee += kThreads) {
-          const int e = ee + lane;
-          const unsigned long long ent = e < cnt ? cur[e] : ~0ull;
-          const float lbe = lb_of(ent);
-          const bool keep = e < cnt && lbe <= thr;
-          const bool take = keep && lbe <= tau;
-          const unsigned m = __ballot_sync(FULL, take);
-          int base = 0;
-          if (m) {
-            const int leader = __ffs(m) - 1;
-            if (lane == leader) base = atomicAdd(&S.take, __popc(m));
-            base = __shfl_sync(FULL, base, leader);
-          }
-          const int slot = base + __popc(m & ((1u << lane) - 1u));
-          const bool got = take && slot < CAP_B;
-          if (got) s_blist[slot] = ent;
-          warp_append(keep && !got, ent, nxt, &S.rem);
-        }
+        filter_list(gl, cnt, S.thr, tau, s_blist, &S.take, gl2, &S.rem);
         __syncthreads();
         const int ntake = S.take < CAP_B ? S.take : CAP_B;
         const int nrem = S.rem;
         bitonic_sort_u64(s_blist, ntake);
         scan_blocks<LT, NF>(A, S, s_blist, ntake, true, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
-        unsigned long long* t = cur;
-        cur = nxt;
-        nxt = t;
-        cnt = nrem;
+        if (nrem > 0) {
+          if (tid == 0) {
+            S.take = 0;
+            S.rem = 0;
+          }
+          __syncthreads();
+          filter_list(gl2, nrem, S.thr, -1.f, s_blist, &S.take, gl, &S.rem);
+          __syncthreads();
+          const int n2 = S.rem;
+          if (n2 <= CAP_B) {
+            for (int i = tid; i < n2; i += kThreads) s_blist[i] = gl[i];
+            __syncthreads();
+            bitonic_sort_u64(s_blist, n2);
+            scan_blocks<LT, NF>(A, S, s_blist, n2, true, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+          } else {
+            scan_blocks<LT, NF>(A, S, gl, n2, false, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+          }
+        }
       }
     }
     // ---------------------------------------------------------------- output
@@ -590,6 +620,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
       atomicAdd(&A.dstats[1], (unsigned long long)A.nb);
       for (int i = 0; i < 10; ++i) atomicAdd(&A.dstats[2 + i], (unsigned long long)S.st[i]);
       for (int i = 0; i < 4; ++i) atomicAdd(&A.dstats[12 + i], (unsigned long long)(t_phase[i + 1] - t_phase[i]));
+      atomicMax(&A.dstats[16], (unsigned long long)(t_phase[4] - t_phase[0]));
+      atomicMax(&A.dstats[17], (unsigned long long)S.st[6]);
+      atomicMax(&A.dstats[18], (unsigned long long)S.st[8]);
     }
     __syncthreads();
   }

@@ -333,6 +333,9 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
     stats->batches = (int64_t)h[10];
     stats->waves = (int64_t)h[11];
     for (int i = 0; i < 4; ++i) stats->phase_cycles[i] = (int64_t)h[12 + i];
+    stats->max_query_cycles = (int64_t)h[16];
+    stats->max_list_blocks = (int64_t)h[17];
+    stats->max_batches = (int64_t)h[18];
   }
   return SOFA_OK;
 }

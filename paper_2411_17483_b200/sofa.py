@@ -57,7 +57,8 @@ class sofa_build_opts(C.Structure):
 class sofa_knn_stats(C.Structure):
     _fields_ = [(f, C.c_int64) for f in ("queries", "blocks_total", "blocks_survived", "words_scanned",
                                          "candidates", "refined", "abandoned", "env_nodes", "list_blocks",
-                                         "rounds", "batches", "waves")] + [("phase_cycles", C.c_int64 * 4)]
+                                         "rounds", "batches", "waves")] + [("phase_cycles", C.c_int64 * 4)] + \
+        [(f, C.c_int64) for f in ("max_query_cycles", "max_list_blocks", "max_batches")]
 
     def to_dict(self) -> dict:
         d = {f: int(getattr(self, f)) for f, _ in self._fields_ if f != "phase_cycles"}
