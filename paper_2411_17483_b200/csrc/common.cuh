@@ -8,6 +8,8 @@
 
 #include "../../include/sofa.h"
 
+#define SOFA_TRACE_FIELDS 16
+
 namespace sofa {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -151,6 +153,10 @@ struct sofa_index {
   int64_t gscratch_ctas = 0;
   int* qcounter = nullptr;
   unsigned long long* dstats = nullptr;
+  long long* trace = nullptr;  // per-query trace (filled when stats are requested)
+  int64_t trace_cap = 0;
+  int trace_on = 0;
+  int32_t trace_q = 0;
   // host-path staging
   float* hq_dev = nullptr;
   float* hd_dev = nullptr;

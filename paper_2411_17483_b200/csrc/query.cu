@@ -54,6 +54,7 @@ struct QArgs {
   int64_t lvl_off[8], lvl_cnt[8];
   int* qcounter;
   unsigned long long* dstats;
+  long long* trace;  // nullable: per query SOFA_TRACE_FIELDS int64
   float weights[SOFA_MAX_L];
 };
 
@@ -624,6 +625,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
       atomicMax(&A.dstats[17], (unsigned long long)S.st[6]);
       atomicMax(&A.dstats[18], (unsigned long long)S.st[8]);
     }
+    if (tid == 0 && A.trace) {
+      long long* tr = A.trace + (int64_t)qi * SOFA_TRACE_FIELDS;
+      for (int i = 0; i < 4; ++i) tr[i] = t_phase[i + 1] - t_phase[i];
+      for (int i = 0; i < 10; ++i) tr[4 + i] = S.st[i];
+      tr[14] = blockIdx.x;
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      tr[15] = smid;
+    }
     __syncthreads();
   }
 }
@@ -688,6 +698,7 @@ int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_
   A.goff = ix->global_offset;
   A.qcounter = ix->qcounter;
   A.dstats = ix->dstats;
+  A.trace = ix->trace_on ? ix->trace : nullptr;
   for (int j = 0; j < SOFA_MAX_L; ++j) A.weights[j] = j < ix->l ? (float)ix->model.weights[j] : 0.f;
   const int nf4 = ix->len / 4;
   const int NF = nf4 <= 32 ? 1 : nf4 <= 64 ? 2 : nf4 <= 128 ? 4 : 8;

@@ -152,7 +152,8 @@ int sofa_learn_model(const float* sample_dev, int64_t S, int32_t len, int32_t l,
 void sofa_free(sofa_index* ix) {
   if (!ix) return;
   void* bufs[] = {ix->words, ix->stats, ix->perm, ix->env, ix->bkey, ix->basis32, ix->basis64, ix->edges32,
-                  ix->edges64, ix->gscratch, ix->qcounter, ix->dstats, ix->hq_dev, ix->hd_dev, ix->hi_dev};
+                  ix->edges64, ix->gscratch, ix->qcounter, ix->dstats, ix->hq_dev, ix->hd_dev, ix->hi_dev,
+                  ix->trace};
   for (void* p : bufs)
     if (p) cudaFree(p);
   delete ix;
@@ -310,6 +311,14 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
   if (!queries_dev || !out_dist_dev || !out_idx_dev) return fail(SOFA_EINVAL, "NULL pointer");
   cudaStream_t st = (cudaStream_t)cuda_stream;
   if (stats) SOFA_CK(cudaMemsetAsync(ix->dstats, 0, 32 * 8, st));
+  ix->trace_on = stats != nullptr;
+  if (stats && ix->trace_cap < q) {
+    if (ix->trace) cudaFree(ix->trace);
+    ix->trace = nullptr;
+    SOFA_CK(cudaMalloc(&ix->trace, (size_t)q * SOFA_TRACE_FIELDS * 8));
+    ix->trace_cap = q;
+  }
+  if (stats) ix->trace_q = q;
   int rc;
   if (ix->n == 0)
     rc = launch_fill_pad(out_dist_dev, out_idx_dev, (int64_t)q * k, st);
@@ -375,6 +384,13 @@ int sofa_merge_topk(const float* dist_dev, const int64_t* idx_dev, int32_t parts
   if (q < 1 || k < 1 || k > SOFA_MAX_K) return fail(SOFA_EINVAL, "bad q / k");
   if (!dist_dev || !idx_dev || !out_dist_dev || !out_idx_dev) return fail(SOFA_EINVAL, "NULL pointer");
   return launch_merge(dist_dev, idx_dev, parts, q, k, out_dist_dev, out_idx_dev, (cudaStream_t)cuda_stream);
+}
+
+int sofa_knn_trace(const sofa_index* ix, int64_t* out_host, int32_t q) {
+  if (!ix || !out_host) return fail(SOFA_EINVAL, "NULL pointer");
+  if (!ix->trace || q != ix->trace_q) return fail(SOFA_EINVAL, "no trace for this q (call sofa_knn with stats first)");
+  SOFA_CK(cudaMemcpy(out_host, ix->trace, (size_t)q * SOFA_TRACE_FIELDS * 8, cudaMemcpyDeviceToHost));
+  return SOFA_OK;
 }
 
 int sofa_get_model(const sofa_index* ix, sofa_model* out) {

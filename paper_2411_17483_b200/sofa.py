@@ -93,6 +93,7 @@ def lib() -> C.CDLL:
         L.sofa_knn_host.argtypes = [VP, VP, I32, I32, VP, VP, P(sofa_knn_stats), VP]
         L.sofa_merge_topk.argtypes = [VP, VP, I32, I32, I32, VP, VP, VP]
         L.sofa_get_model.argtypes = [VP, P(sofa_model)]
+        L.sofa_knn_trace.argtypes = [VP, VP, I32]
         L.sofa_transform.argtypes = [VP, I64, P(sofa_model), VP, VP, VP]
         L.sofa_get_info.argtypes = [VP, P(sofa_index_info)]
         L.sofa_export_index.argtypes = [VP, VP, VP, VP, VP, VP]
@@ -163,6 +164,17 @@ def sofa_knn_host(ix, queries_host, q, k, out_dist_host, out_idx_host, stats=Non
 def sofa_merge_topk(dist_dev, idx_dev, parts, q, k, out_dist_dev, out_idx_dev, stream=None):
     _ck(lib().sofa_merge_topk(_ptr(dist_dev), _ptr(idx_dev), parts, q, k, _ptr(out_dist_dev), _ptr(out_idx_dev),
                               _stream(stream)))
+
+
+TRACE_FIELDS = ("cyc_prep", "cyc_seed", "cyc_tree", "cyc_scan", "blocks_survived", "words_scanned",
+                "candidates", "refined", "abandoned", "env_nodes", "list_blocks", "rounds", "batches", "waves",
+                "cta", "sm")
+
+
+def sofa_knn_trace(ix, q) -> np.ndarray:
+    out = np.zeros((q, len(TRACE_FIELDS)), dtype=np.int64)
+    _ck(lib().sofa_knn_trace(ix, out.ctypes.data, q))
+    return out
 
 
 def sofa_get_model(ix) -> sofa_model:
