@@ -100,53 +100,60 @@ __device__ __forceinline__ void warp_append(bool pass, unsigned long long key, u
 }
 
 struct QShared {
-  int qi, cnt, ncand, tkn, b0, take, rem;
+  int qi, cnt, ncand, tkn, b0, take, rem, next, lock;
   float bsf, bsf_init, thr;
   // per query: 0 blocks_survived, 1 words_scanned, 2 candidates, 3 refined, 4 abandoned, 5 env_nodes,
   // 6 list_blocks, 7 rounds, 8 batches, 9 waves
   unsigned int st[10];
 };
 
-// exact squared z-ED with early abandoning (a8): one warp, float4 loads, chunk = 2 float4 / lane
-template <int NF>
-__device__ __forceinline__ float ed_warp(const float* __restrict__ row, float2 st, const float4* s_qh4, int nf4,
-                                         float bsf, bool& abandoned) {
+// exact squared z-ED with early abandoning (a8) for R candidate rows at once: one warp, float4
+// loads of all R rows issued together (R rows in flight per warp), chunks of 2 float4 per lane
+// (256 values), partial sums warp-reduced after each chunk and compared with the BSF.
+template <int NF, int R>
+__device__ __forceinline__ void ed_warp_multi(const float* const (&rows)[R], const float2 (&st)[R],
+                                              const bool (&on)[R], const float4* s_qh4, int nf4, float bsf,
+                                              float (&d2)[R], bool (&ab)[R]) {
   const int lane = threadIdx.x & 31;
-  const float4* r4 = reinterpret_cast<const float4*>(row);
-  float total = 0.f;
-  abandoned = false;
   constexpr int CH = NF < 2 ? NF : 2;
 #pragma unroll
+  for (int r = 0; r < R; ++r) {
+    d2[r] = 0.f;
+    ab[r] = false;
+  }
+#pragma unroll
   for (int f0 = 0; f0 < NF; f0 += CH) {
-    float4 x[CH];
+    float4 x[R][CH];
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      const int fi = lane + 32 * (f0 + c);
-      x[c] = fi < nf4 ? ld_stream(r4 + fi) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    float acc = 0.f;
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      const int fi = lane + 32 * (f0 + c);
-      if (fi < nf4) {
-        const float4 q = s_qh4[fi];
-        const float d0 = __fsub_rn(__fmul_rn(__fsub_rn(x[c].x, st.x), st.y), q.x);
-        const float d1 = __fsub_rn(__fmul_rn(__fsub_rn(x[c].y, st.x), st.y), q.y);
-        const float d2 = __fsub_rn(__fmul_rn(__fsub_rn(x[c].z, st.x), st.y), q.z);
-        const float d3 = __fsub_rn(__fmul_rn(__fsub_rn(x[c].w, st.x), st.y), q.w);
-        acc = __fmaf_rn(d0, d0, acc);
-        acc = __fmaf_rn(d1, d1, acc);
-        acc = __fmaf_rn(d2, d2, acc);
-        acc = __fmaf_rn(d3, d3, acc);
+      for (int c = 0; c < CH; ++c) {
+        const int fi = lane + 32 * (f0 + c);
+        x[r][c] = (on[r] && !ab[r] && fi < nf4) ? ld_stream(reinterpret_cast<const float4*>(rows[r]) + fi)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-    }
-    total += warp_sum_f32(acc);
-    if (f0 + CH < NF && total > bsf) {
-      abandoned = true;
-      return total;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int fi = lane + 32 * (f0 + c);
+        if (fi < nf4) {
+          const float4 q = s_qh4[fi];
+          const float e0 = __fsub_rn(__fmul_rn(__fsub_rn(x[r][c].x, st[r].x), st[r].y), q.x);
+          const float e1 = __fsub_rn(__fmul_rn(__fsub_rn(x[r][c].y, st[r].x), st[r].y), q.y);
+          const float e2 = __fsub_rn(__fmul_rn(__fsub_rn(x[r][c].z, st[r].x), st[r].y), q.z);
+          const float e3 = __fsub_rn(__fmul_rn(__fsub_rn(x[r][c].w, st[r].x), st[r].y), q.w);
+          acc = __fmaf_rn(e0, e0, acc);
+          acc = __fmaf_rn(e1, e1, acc);
+          acc = __fmaf_rn(e2, e2, acc);
+          acc = __fmaf_rn(e3, e3, acc);
+        }
+      }
+      d2[r] += warp_sum_f32(acc);
+      if (f0 + CH < NF && d2[r] > bsf) ab[r] = true;
     }
   }
-  return total;
 }
 
 // word LB (d_SFA^2 from the T table) with chunked early abandoning: Alg. 3.  The word's
@@ -159,78 +166,127 @@ __device__ __forceinline__ float word_lb(const uint4 (&w)[LT / 16], const float*
     const uint32_t wv[4] = {w[c].x, w[c].y, w[c].z, w[c].w};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {  // two chunks of 8 positions per 16 bytes
+      float t[8];
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) {
         const int j = c * 16 + h * 8 + jj;
         const uint32_t sym = (wv[(h * 8 + jj) >> 2] >> (8 * (jj & 3))) & 0xffu;
-        lb += sT[j * 256 + sym];
+        t[jj] = sT[j * 256 + sym];
       }
+      // pairwise sum: dependency depth 3 instead of 8 (LB rounding is absorbed by thr's slack)
+      lb += ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
       if (lb > thr) return lb;
     }
   }
   return lb;
 }
 
+// top-k insertion under a shared-memory spin lock (one lane of one warp at a time); updates the
+// BSF (k-th best squared distance, or the caller's bound) and the pruning threshold.
+__device__ void topk_insert(const QArgs& A, QShared& S, float* s_tkd, int* s_tki, float d, int i) {
+  if (d > S.bsf_init) return;  // above the caller's bound: never part of the answer
+  while (atomicCAS(&S.lock, 0, 1) != 0) {
+  }
+  __threadfence_block();
+  const int k = A.k;
+  const int n = S.tkn;
+  if (n < k || d < s_tkd[n - 1] || (d == s_tkd[n - 1] && i < s_tki[n - 1])) {
+    int p = n < k ? n : k - 1;
+    while (p > 0 && (s_tkd[p - 1] > d || (s_tkd[p - 1] == d && s_tki[p - 1] > i))) {
+      s_tkd[p] = s_tkd[p - 1];
+      s_tki[p] = s_tki[p - 1];
+      --p;
+    }
+    s_tkd[p] = d;
+    s_tki[p] = i;
+    if (n < k) S.tkn = n + 1;
+    if (S.tkn == k) {
+      const float b = fminf(S.bsf_init, s_tkd[k - 1]);
+      *(volatile float*)&S.bsf = b;
+      *(volatile float*)&S.thr = thr_of(b);
+    }
+  }
+  __threadfence_block();
+  atomicExch(&S.lock, 0);
+}
+
+// a8: refine the candidate buffer.  Candidates are bitonic-sorted by LB when there are more than
+// 8; then every warp independently pulls the next R candidates in ascending-LB order (atomic
+// counter), skips those whose LB exceeds the current threshold (and stops, the list being
+// sorted), computes their exact distances with R rows in flight, and inserts improvements into
+// the top-k.  No CTA-wide barrier per candidate wave.
 template <int LT, int NF>
 __device__ void refine_candidates(const QArgs& A, QShared& S, unsigned long long* s_cand, float* s_tkd, int* s_tki,
-                                  float* s_wd, int* s_wi, const float4* s_qh4) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+                                  const float4* s_qh4) {
+  constexpr int R = NF <= 2 ? 2 : 1;  // rows in flight per warp
+  const int tid = threadIdx.x, lane = tid & 31;
   const int nc = S.ncand;
   if (nc == 0) return;
-  if (nc > 8) bitonic_sort_u64(s_cand, nc);
+  const bool sorted = nc > 8;
+  if (sorted) bitonic_sort_u64(s_cand, nc);
   const int nf4 = A.len >> 2;
-  for (int base = 0; base < nc; base += 8) {
-    const float thr = S.thr, bsf = S.bsf;
-    const int c = base + warp;
-    float d2 = INFINITY;
-    int oidx = -1;
-    bool did = false, ab = false;
-    if (c < nc) {
-      const unsigned long long e = s_cand[c];
-      if (lb_of(e) <= thr) {
-        did = true;
+  unsigned int n_ref = 0, n_ab = 0, n_waves = 0;
+  for (;;) {
+    int c0 = 0;
+    if (lane == 0) c0 = atomicAdd(&S.next, R);
+    c0 = __shfl_sync(FULL, c0, 0);
+    if (c0 >= nc) break;
+    const float thr = *(volatile float*)&S.thr;
+    const float bsf = *(volatile float*)&S.bsf;
+    const float* rows[R];
+    float2 st[R];
+    bool on[R];
+    int oidx[R];
+    bool any = false;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int c = c0 + r;
+      const unsigned long long e = c < nc ? s_cand[c] : ~0ull;
+      on[r] = c < nc && lb_of(e) <= thr;
+      oidx[r] = -1;
+      rows[r] = A.series;
+      st[r] = make_float2(0.f, 0.f);
+      if (on[r]) {
         const uint32_t pos = (uint32_t)e;
-        oidx = A.perm[pos];
-        const float2 st = A.stats[pos];
-        d2 = ed_warp<NF>(A.series + (int64_t)oidx * A.len, st, s_qh4, nf4, bsf, ab);
+        oidx[r] = A.perm[pos];
+        st[r] = A.stats[pos];
+        rows[r] = A.series + (int64_t)oidx[r] * A.len;
+        any = true;
       }
     }
-    if (tid == 0) S.st[9] += 1;
+    if (!any) {
+      if (sorted) break;  // every later candidate has a larger LB
+      continue;
+    }
+    float d2[R];
+    bool ab[R];
+    ed_warp_multi<NF, R>(rows, st, on, s_qh4, nf4, bsf, d2, ab);
+    ++n_waves;
     if (lane == 0) {
-      s_wd[warp] = (did && !ab) ? d2 : INFINITY;
-      s_wi[warp] = (did && !ab) ? oidx : -1;
-      if (did) atomicAdd(&S.st[3], 1u);
-      if (ab) atomicAdd(&S.st[4], 1u);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      const int k = A.k;
-      for (int w = 0; w < 8; ++w) {
-        const int i = s_wi[w];
-        if (i < 0) continue;
-        const float d = s_wd[w];
-        if (d > S.bsf_init) continue;  // above the caller's bound: never part of the answer
-        const int n = S.tkn;
-        if (n < k || d < s_tkd[n - 1] || (d == s_tkd[n - 1] && i < s_tki[n - 1])) {
-          int p = n < k ? n : k - 1;
-          while (p > 0 && (s_tkd[p - 1] > d || (s_tkd[p - 1] == d && s_tki[p - 1] > i))) {
-            s_tkd[p] = s_tkd[p - 1];
-            s_tki[p] = s_tki[p - 1];
-            --p;
-          }
-          s_tkd[p] = d;
-          s_tki[p] = i;
-          if (n < k) S.tkn = n + 1;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!on[r]) continue;
+        ++n_ref;
+        if (ab[r]) {
+          ++n_ab;
+          continue;
         }
+        const int n = *(volatile int*)&S.tkn;
+        const float kd = *(volatile float*)&s_tkd[n > 0 ? n - 1 : 0];
+        if (n < A.k || d2[r] <= kd) topk_insert(A, S, s_tkd, s_tki, d2[r], oidx[r]);
       }
-      if (S.tkn == k) S.bsf = fminf(S.bsf_init, s_tkd[k - 1]);
-      S.thr = thr_of(S.bsf);
     }
-    __syncthreads();
-    if (base + 8 < nc && lb_of(s_cand[base + 8]) > S.thr) break;
+  }
+  if (lane == 0) {
+    if (n_ref) atomicAdd(&S.st[3], n_ref);
+    if (n_ab) atomicAdd(&S.st[4], n_ab);
+    if (n_waves) atomicAdd(&S.st[9], n_waves);
   }
   __syncthreads();
-  if (tid == 0) S.ncand = 0;
+  if (tid == 0) {
+    S.ncand = 0;
+    S.next = 0;
+  }
   __syncthreads();
 }
 
@@ -303,7 +359,7 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
     if ((tid & 31) == 0 && scanned) atomicAdd(&S.st[1], scanned);
     __syncthreads();
     if (tid == 0) S.st[2] += S.ncand;
-    refine_candidates<LT, NF>(A, S, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+    refine_candidates<LT, NF>(A, S, s_cand, s_tkd, s_tki, s_qh4);
   }
 }
 
@@ -472,6 +528,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
         S.cnt = 0;
         S.ncand = 0;
         S.tkn = 0;
+        S.next = 0;
+        S.lock = 0;
         for (int i = 0; i < 10; ++i) S.st[i] = 0;
         const float bi = A.bsf_init ? A.bsf_init[qi] : INFINITY;
         S.bsf_init = bi;
