@@ -231,8 +231,15 @@ __device__ void refine_candidates(const QArgs& A, QShared& S, unsigned long long
     if (lane == 0) c0 = atomicAdd(&S.next, R);
     c0 = __shfl_sync(FULL, c0, 0);
     if (c0 >= nc) break;
-    const float thr = *(volatile float*)&S.thr;
-    const float bsf = *(volatile float*)&S.bsf;
+    // lane 0 reads the (concurrently updated) threshold and broadcasts it: every lane must take
+    // the same branch below, since ed_warp_multi uses full-warp shuffles
+    float thr = 0.f, bsf = 0.f;
+    if (lane == 0) {
+      thr = *(volatile float*)&S.thr;
+      bsf = *(volatile float*)&S.bsf;
+    }
+    thr = __shfl_sync(FULL, thr, 0);
+    bsf = __shfl_sync(FULL, bsf, 0);
     const float* rows[R];
     float2 st[R];
     bool on[R];

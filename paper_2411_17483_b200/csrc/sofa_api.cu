@@ -4,6 +4,7 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
