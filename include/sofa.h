@@ -78,7 +78,14 @@ typedef struct {
   int32_t block_size;      /* B series per leaf block, default 256 (reading 19) */
   int32_t candidate_limit; /* max complex index eligible for selection; 0 => n/2 (reading 3) */
   int32_t binning;         /* SOFA_BINNING_EQUI_DEPTH (default) or _EQUI_WIDTH */
-  int32_t reserved;
+  int32_t dense_permille;  /* dense path for a query whose leaf list still keeps
+                              >= this many permille of the blocks after its 8 lowest-LB leaves
+                              were refined and >= 1/16 of their words still pass the tightened
+                              bound; the batch runs the tensor-core pass only if the flagged
+                              queries' estimated refines add up to one pass over the rows (else a
+                              second sparse launch finishes them).  0 => 100 (10%), < 0 => never,
+                              >= 1000 => every query with a surviving leaf (testing).  Results are
+                              identical either way; only speed changes. */
   int64_t global_offset;   /* global index of this shard's row 0 (0 on one GPU) */
   int64_t global_n;        /* total rows over all shards (0 => this call's n) */
   const sofa_model* model; /* nullable: NULL => learn from this call's rows at the global
@@ -102,6 +109,11 @@ typedef struct {
   int64_t max_query_cycles; /* slowest query (SM cycles) */
   int64_t max_list_blocks;  /* largest per-query leaf list */
   int64_t max_batches;      /* most word-scan batches of one query */
+  int64_t dense_queries;    /* queries finished by the dense path (tensor-core screen + exact refine) */
+  int64_t dense_candidates; /* (query, row) pairs the dense screen passed to the exact refine */
+  int64_t dense_refined;    /* exact distances computed by the dense path (incl. fallback rescans) */
+  int64_t scan_tasks;       /* leaf chunks the front published to the scan pool (spread over all CTAs) */
+  int64_t scan_queries;     /* queries that published at least one scan task */
 } sofa_knn_stats;
 
 /* Fill *out with defaults (sample_ratio 0.01, block_size 256, equi-depth, everything else 0). */
@@ -129,9 +141,14 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
                const sofa_build_opts* opts, void* cuda_stream, sofa_index** out);
 
 /* sofa_knn(queries, q, k) — BASELINE.json north_star call; exact k-NN under z-ED.
- * One fused persistent kernel: per query a5 tables -> a6 own-key-block seed and envelope LB
- * scan -> a7 word LB scan (chunks of 8, abandon) -> a8 LB-ordered refine with early
- * abandoning and top-k.
+ * Three stream-ordered launches, no host synchronisation: (1) the front, one CTA per query at a
+ * time: a5 tables -> a6 own-key-block seed and envelope-tree descent -> the 8 lowest-LB leaves
+ * (a7 word LB scan in chunks of 8 with abandoning, a8 LB-ordered refine with early abandoning
+ * and top-k) -> the rest of the leaf list published as scan tasks; a query the SFA bound
+ * cannot prune is flagged for (2) the dense pass (tensor-core TF32 screen with a proven error
+ * bound + exact refine) if the flagged queries justify a full pass; (3) the scan
+ * pass: every CTA pulls tasks of any query (a7 + a8 against the query's shared top-k); the CTA
+ * finishing a query's last task writes its result.
  *   queries_dev: q x len float32 device (raw; z-normalised inside).
  *   bsf_init_dev: nullable, q floats: an upper bound on each query's k-th squared distance
  *   (e.g. from another shard) used to prune; results above it may be absent (padding).
@@ -152,10 +169,11 @@ int sofa_knn_host(sofa_index* ix, const float* queries_host, int32_t q, int32_t 
 int sofa_merge_topk(const float* dist_dev, const int64_t* idx_dev, int32_t parts, int32_t q, int32_t k,
                     float* out_dist_dev, int64_t* out_idx_dev, void* cuda_stream);
 
-/* Per-query trace of the last sofa_knn call made WITH `stats` on this index: q rows of 16 int64
+/* Per-query trace of the last sofa_knn call made WITH `stats` on this index: q rows of 20 int64
  * (SM cycles of prep+tables, seed, tree, scan+refine; blocks_survived, words_scanned, candidates,
- * refined, abandoned, env_nodes, list_blocks, rounds, batches, waves; CTA id; SM id), copied to
- * out_host (q x 16).  Errors: EINVAL if no such trace. */
+ * refined, abandoned, env_nodes, list_blocks, rounds, batches, waves; CTA id; SM id; dense-path
+ * decision inputs: flagged, leaves after the take round, take-word passes, take words), copied to
+ * out_host (q x 20).  Errors: EINVAL if no such trace. */
 int sofa_knn_trace(const sofa_index* ix, int64_t* out_host, int32_t q);
 
 /* Copy the index's model to *out (host). */

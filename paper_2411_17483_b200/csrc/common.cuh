@@ -8,7 +8,7 @@
 
 #include "../../include/sofa.h"
 
-#define SOFA_TRACE_FIELDS 16
+#define SOFA_TRACE_FIELDS 20
 
 namespace sofa {
 
@@ -102,6 +102,55 @@ __device__ __forceinline__ void row_stats(const float4 (&x)[NF], int nf4, int le
   inv64 = sd < 1e-12 ? 0.0 : 1.0 / sd;
 }
 
+// exact squared z-ED with early abandoning (a8) for R candidate rows at once: one warp, float4
+// loads of all R rows issued together (R rows in flight per warp), chunks of 2 float4 per lane
+// (256 values), partial sums warp-reduced after each chunk and compared with the BSF.
+template <int NF, int R>
+__device__ __forceinline__ void ed_warp_multi(const float* const (&rows)[R], const float2 (&st)[R],
+                                              const bool (&on)[R], const float4* s_qh4, int nf4, float bsf,
+                                              float (&d2)[R], bool (&ab)[R]) {
+  const int lane = threadIdx.x & 31;
+  constexpr int CH = (NF < 2 || R >= 8) ? 1 : 2;  // float4 per lane per chunk (8 rows in flight: 1)
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    d2[r] = 0.f;
+    ab[r] = false;
+  }
+#pragma unroll
+  for (int f0 = 0; f0 < NF; f0 += CH) {
+    float4 x[R][CH];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int fi = lane + 32 * (f0 + c);
+        x[r][c] = (on[r] && !ab[r] && fi < nf4) ? ld_stream(reinterpret_cast<const float4*>(rows[r]) + fi)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int fi = lane + 32 * (f0 + c);
+        if (fi < nf4) {
+          const float4 q = s_qh4[fi];
+          const float e0 = __fsub_rn(__fmul_rn(__fsub_rn(x[r][c].x, st[r].x), st[r].y), q.x);
+          const float e1 = __fsub_rn(__fmul_rn(__fsub_rn(x[r][c].y, st[r].x), st[r].y), q.y);
+          const float e2 = __fsub_rn(__fmul_rn(__fsub_rn(x[r][c].z, st[r].x), st[r].y), q.z);
+          const float e3 = __fsub_rn(__fmul_rn(__fsub_rn(x[r][c].w, st[r].x), st[r].y), q.w);
+          acc = __fmaf_rn(e0, e0, acc);
+          acc = __fmaf_rn(e1, e1, acc);
+          acc = __fmaf_rn(e2, e2, acc);
+          acc = __fmaf_rn(e3, e3, acc);
+        }
+      }
+      d2[r] += warp_sum_f32(acc);
+      if (f0 + CH < NF && d2[r] > bsf) ab[r] = true;
+    }
+  }
+}
+
 // upper_bound over a 256-entry edge row padded with +inf: number of edges <= v (symbol of v;
 // bins [beta(s), beta(s+1)) — P:225-228, value on an edge goes right).
 template <typename E>
@@ -131,6 +180,28 @@ __device__ __forceinline__ uint64_t word_key(const uint8_t* w, int l, int a_bits
 
 }  // namespace sofa
 
+// Dense-path (f1) scratch, per index, grown on demand (dense.cu).  counters (16 ints):
+// [0] dense query slots, [1] overflowed slots, [2..3] candidate count (u64), [4] finished CTAs,
+// [6..7] estimated sparse refines of the flagged queries (u64, the batch decision).
+struct DenseScratch {
+  int q_cap = 0, k_cap = 0, len = 0;
+  int64_t cand_cap = 0;
+  float* qhat = nullptr;      // slot x len: z-normalised query (float32, same bits as the sparse path)
+  float4* qparams = nullptr;  // slot: (|q^|^2, sum q^, 2 gamma |q^|, refine slack)
+  int* qidx = nullptr;        // slot -> query index
+  float* binit = nullptr;     // slot -> caller's bound
+  float* bsf = nullptr;       // slot -> exact k-th best squared distance (or the bound)
+  float* thr = nullptr;       // slot -> screening threshold
+  float* tkd = nullptr;       // slot x k_cap
+  int* tki = nullptr;         // slot x k_cap (local rows)
+  int* tkn = nullptr;
+  int* lock = nullptr;
+  int* overflow = nullptr;
+  int* ovf_list = nullptr;
+  unsigned long long* cand = nullptr;
+  int* counters = nullptr;
+};
+
 // Host-side index object (opaque in the C ABI).
 struct sofa_index {
   int64_t n = 0, nb = 0, global_offset = 0, global_n = 0;
@@ -139,6 +210,9 @@ struct sofa_index {
   const float* series = nullptr;  // borrowed
   uint8_t* words = nullptr;       // n x WS, sorted by key
   float2* stats = nullptr;        // n, sorted order: (mu, 1/sigma)
+  float2* stats_orig = nullptr;   // n, original row order (dense path)
+  int32_t dense_permille = 100;   // dense path when >= this many permille of blocks survive (0: off)
+  DenseScratch dense;
   int32_t* perm = nullptr;        // n: sorted position -> local row
   uint8_t* env = nullptr;         // nb x 2 x WS
   uint64_t* bkey = nullptr;       // nb first keys
@@ -152,6 +226,11 @@ struct sofa_index {
   unsigned long long* gscratch = nullptr;
   int64_t gscratch_ctas = 0;
   int* qcounter = nullptr;
+  // front/scan split (query.cu): per-query state, tables, the leaf pool and the scan tasks
+  void *qstate = nullptr, *q_T = nullptr, *q_hat = nullptr, *pool = nullptr, *tasks = nullptr,
+       *rank_count = nullptr;
+  int64_t scan_q_cap = 0, pool_cap = 0, task_cap = 0, rank_cap = 0;
+  int scan_LT = 0;
   unsigned long long* dstats = nullptr;
   long long* trace = nullptr;  // per-query trace (filled when stats are requested)
   int64_t trace_cap = 0;
@@ -178,7 +257,13 @@ int launch_gather(const uint8_t* words, const float2* stats, const int32_t* perm
 int learn_model_dev(const float* sample, int64_t S, int len, int l, int a, int binning, int cand_limit,
                     cudaStream_t st, sofa_model* out);
 int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
-                 cudaStream_t st);
+                 cudaStream_t st, bool scan = false);
+// batch-level dense decision (f1): run the tensor-core pass iff the flagged queries' estimated sparse
+// refines add up to at least one full pass over the shard's rows
+inline int64_t dense_batch_rows(const sofa_index* ix) { return ix->n > 0 ? ix->n : 1; }
+int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stats, cudaStream_t st);
+int ensure_dense_scratch(sofa_index* ix, int q, int k);
+void free_dense_scratch(sofa_index* ix);
 int launch_merge(const float* d, const int64_t* i, int parts, int q, int k, float* od, int64_t* oi, cudaStream_t st);
 int launch_fill_pad(float* od, int64_t* oi, int64_t cnt, cudaStream_t st);
 }  // namespace sofa

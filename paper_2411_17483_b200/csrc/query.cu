@@ -23,14 +23,38 @@
 //       exceeds the threshold.
 // thr = BSF * (1 + 1e-4) + 1e-5 (squared units): prune only when the float32 lower bound clearly
 // exceeds the float32 k-th best; this absorbs the data-side projection error (reading 15).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace sofa {
 
 constexpr int CAP_B = 2048;  // surviving blocks sorted in shared memory
-constexpr int CAP_C = 2048;  // words per scan batch = candidate buffer capacity
+constexpr int CAP_C = 2048;  // words per scan batch (l <= 16)
+constexpr int CAPC = 4096;   // candidate buffer: one batch + candidates pending from earlier batches
 constexpr int KMAX = SOFA_MAX_K;
 constexpr int kFan = 16;  // envelope tree fan-out
+
+// Front / scan split.  The front mode of k_query does the per-query steps (a5 tables, a6 seed and
+// envelope descent, the TAKE_F lowest-LB leaves, the dense-path decision) and publishes the rest of
+// the query's leaf list as scan tasks (chunks of leaves) into a global pool; the scan mode spreads
+// all queries' tasks over all CTAs, so a heavy query no longer sits on one CTA.  A query's top-k
+// lives in its QState while tasks are in flight; the CTA that finishes its last task writes the
+// output.  Results do not depend on which CTA scans which chunk.
+struct QState {
+  int tkn, lock, ntasks, done;
+  float bsf, bsf_init;
+  float tkd[SOFA_MAX_K];
+  int tki[SOFA_MAX_K];
+};
+struct ScanTask {
+  int64_t off;  // into the leaf pool
+  int q;
+  int cnt_flags;  // leaves | sorted << 30 | dense candidate << 29
+  int rank;       // position in the query's LB-ordered chunk sequence
+  int pad;
+};
+constexpr int kTaskSorted = 1 << 30, kTaskDense = 1 << 29, kTaskCnt = (1 << 29) - 1;
 
 struct QArgs {
   const float* series;
@@ -55,6 +79,31 @@ struct QArgs {
   int* qcounter;
   unsigned long long* dstats;
   long long* trace;  // nullable: per query SOFA_TRACE_FIELDS int64
+  // dense path (f1, dense.cu): a query whose leaf list keeps >= dense_min blocks after its
+  // TAKE0 (8) lowest-LB blocks were refined is handed over (0 = never)
+  int64_t dense_min;
+  int64_t dense_rows;  // batch decision: dense pass iff the flagged queries' estimated refines >= this
+  int dense_force;     // dense_permille >= 1000: every query with a surviving leaf goes dense (tests)
+  int mode;            // 0: front, 1: scan
+  int front_batches;   // word batches of LB-ordered leaves the front scans itself per query
+  QState* qs;          // q
+  float* q_T;          // q x LT x 256 word-LB tables
+  float* q_hat;        // q x len z-normalised queries
+  unsigned long long* pool;  // q x nb leaf entries (LB, block)
+  unsigned long long* pool_used;
+  // two task sets, rank-major: tasks[s][r * q + i] = i-th chunk of rank r (a query's r-th lowest-LB
+  // chunk) in set s; set 0 = ordinary queries, set 1 = dense candidates (scanned only if the batch
+  // skips the dense pass)
+  ScanTask* tasks;     // 2 x rank_cap x q
+  int* rank_count;     // 2 x rank_cap
+  int rank_cap;
+  int* counters;       // [2s] ranks used in set s, [2s+1] its cursor
+  int* qd_counter;
+  float* d_qhat;
+  float4* d_qparams;
+  int* d_qidx;
+  float *d_binit, *d_bsf, *d_thr, *d_tkd;
+  int *d_tki, *d_tkn, *d_lock, *d_overflow;
   float weights[SOFA_MAX_L];
 };
 
@@ -100,61 +149,13 @@ __device__ __forceinline__ void warp_append(bool pass, unsigned long long key, u
 }
 
 struct QShared {
-  int qi, cnt, ncand, tkn, b0, take, rem, next, lock;
+  int qi, cnt, ncand, tkn, b0, take, rem, next, lock, gslot, chunk, ntask, p1, p2;
+  long long off;
   float bsf, bsf_init, thr;
   // per query: 0 blocks_survived, 1 words_scanned, 2 candidates, 3 refined, 4 abandoned, 5 env_nodes,
   // 6 list_blocks, 7 rounds, 8 batches, 9 waves
   unsigned int st[10];
 };
-
-// exact squared z-ED with early abandoning (a8) for R candidate rows at once: one warp, float4
-// loads of all R rows issued together (R rows in flight per warp), chunks of 2 float4 per lane
-// (256 values), partial sums warp-reduced after each chunk and compared with the BSF.
-template <int NF, int R>
-__device__ __forceinline__ void ed_warp_multi(const float* const (&rows)[R], const float2 (&st)[R],
-                                              const bool (&on)[R], const float4* s_qh4, int nf4, float bsf,
-                                              float (&d2)[R], bool (&ab)[R]) {
-  const int lane = threadIdx.x & 31;
-  constexpr int CH = NF < 2 ? NF : 2;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    d2[r] = 0.f;
-    ab[r] = false;
-  }
-#pragma unroll
-  for (int f0 = 0; f0 < NF; f0 += CH) {
-    float4 x[R][CH];
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const int fi = lane + 32 * (f0 + c);
-        x[r][c] = (on[r] && !ab[r] && fi < nf4) ? ld_stream(reinterpret_cast<const float4*>(rows[r]) + fi)
-                                                : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      float acc = 0.f;
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const int fi = lane + 32 * (f0 + c);
-        if (fi < nf4) {
-          const float4 q = s_qh4[fi];
-          const float e0 = __fsub_rn(__fmul_rn(__fsub_rn(x[r][c].x, st[r].x), st[r].y), q.x);
-          const float e1 = __fsub_rn(__fmul_rn(__fsub_rn(x[r][c].y, st[r].x), st[r].y), q.y);
-          const float e2 = __fsub_rn(__fmul_rn(__fsub_rn(x[r][c].z, st[r].x), st[r].y), q.z);
-          const float e3 = __fsub_rn(__fmul_rn(__fsub_rn(x[r][c].w, st[r].x), st[r].y), q.w);
-          acc = __fmaf_rn(e0, e0, acc);
-          acc = __fmaf_rn(e1, e1, acc);
-          acc = __fmaf_rn(e2, e2, acc);
-          acc = __fmaf_rn(e3, e3, acc);
-        }
-      }
-      d2[r] += warp_sum_f32(acc);
-      if (f0 + CH < NF && d2[r] > bsf) ab[r] = true;
-    }
-  }
-}
 
 // word LB (d_SFA^2 from the T table) with chunked early abandoning: Alg. 3.  The word's
 // 16-byte chunks were loaded beforehand (all loads of a batch are in flight together).
@@ -185,6 +186,40 @@ __device__ __forceinline__ float word_lb(const uint4 (&w)[LT / 16], const float*
 // BSF (k-th best squared distance, or the caller's bound) and the pruning threshold.
 __device__ void topk_insert(const QArgs& A, QShared& S, float* s_tkd, int* s_tki, float d, int i) {
   if (d > S.bsf_init) return;  // above the caller's bound: never part of the answer
+  if (S.gslot >= 0) {          // scan mode: the query's top-k lives in its QState
+    QState* h = &A.qs[S.gslot];
+    while (atomicCAS(&h->lock, 0, 1) != 0) {
+    }
+    __threadfence();
+    volatile float* td = h->tkd;
+    volatile int* ti = h->tki;
+    const int k = A.k;
+    const int n = *(volatile int*)&h->tkn;
+    float b = INFINITY;
+    if (n < k || d < td[n - 1] || (d == td[n - 1] && i < ti[n - 1])) {
+      int p = n < k ? n : k - 1;
+      while (p > 0 && (td[p - 1] > d || (td[p - 1] == d && ti[p - 1] > i))) {
+        td[p] = td[p - 1];
+        ti[p] = ti[p - 1];
+        --p;
+      }
+      td[p] = d;
+      ti[p] = i;
+      const int nn = n < k ? n + 1 : k;
+      *(volatile int*)&h->tkn = nn;
+      if (nn == k) {
+        b = fminf(S.bsf_init, td[k - 1]);
+        *(volatile float*)&h->bsf = b;
+      }
+    }
+    __threadfence();
+    atomicExch(&h->lock, 0);
+    if (b < INFINITY) {  // local mirror of the BSF (monotone: atomicMin on the bit patterns)
+      atomicMin(reinterpret_cast<unsigned int*>(&S.bsf), __float_as_uint(b));
+      atomicMin(reinterpret_cast<unsigned int*>(&S.thr), __float_as_uint(thr_of(b)));
+    }
+    return;
+  }
   while (atomicCAS(&S.lock, 0, 1) != 0) {
   }
   __threadfence_block();
@@ -210,164 +245,291 @@ __device__ void topk_insert(const QArgs& A, QShared& S, float* s_tkd, int* s_tki
   atomicExch(&S.lock, 0);
 }
 
-// a8: refine the candidate buffer.  Candidates are bitonic-sorted by LB when there are more than
-// 8; then every warp independently pulls the next R candidates in ascending-LB order (atomic
-// counter), skips those whose LB exceeds the current threshold (and stops, the list being
-// sorted), computes their exact distances with R rows in flight, and inserts improvements into
-// the top-k.  No CTA-wide barrier per candidate wave.
+// a7 + a8 over a list of leaves, barrier-free and warp-centric.  Each warp pulls the next unit (a
+// leaf, or a part of one) from a shared counter — in ascending leaf LB when the list is sorted, and
+// stopping at the first leaf whose LB exceeds the BSF (MESSI's priority order and stop rule,
+// P:173-176) — loads its words with 128-bit loads, computes their LBs from the shared-memory table
+// (Alg. 3, chunks of 8 positions with early abandoning), then refines its candidates in ascending
+// LB: R at a time (the R smallest by warp-min extraction), exact squared ED with early abandoning
+// (P:382), improvements into the shared top-k.  The BSF every warp reads is the shared one, so a
+// warp's improvement prunes the other warps' candidates at once; no CTA barrier inside the loop.
 template <int LT, int NF>
-__device__ void refine_candidates(const QArgs& A, QShared& S, unsigned long long* s_cand, float* s_tkd, int* s_tki,
-                                  const float4* s_qh4) {
-  constexpr int R = NF <= 2 ? 2 : 1;  // rows in flight per warp
+__device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long* list, int cnt, bool sorted,
+                            const float* s_T, float* s_tkd, int* s_tki, const float4* s_qh4) {
+  constexpr int NC = LT / 16;
+  constexpr int WMAX = 8 / NC;                          // words per lane per unit
+  constexpr int R = NF <= 2 ? 4 : (NF <= 4 ? 2 : 1);  // rows refined together per warp
+  constexpr int NW = kThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int nc = S.ncand;
-  if (nc == 0) return;
-  const bool sorted = nc > 8;
-  if (sorted) bitonic_sort_u64(s_cand, nc);
+  if (cnt <= 0) return;
+  const int B = A.B;
+  int ppl = B / (32 * WMAX);  // units per leaf
+  if (ppl < 1) ppl = 1;
+  while (ppl * 2 <= B / 32 && cnt * ppl < 2 * NW) ppl *= 2;  // short lists: split leaves over the warps
+  const int span = B / ppl, wpl = span / 32;
+  const int units = cnt * ppl;
   const int nf4 = A.len >> 2;
-  unsigned int n_ref = 0, n_ab = 0, n_waves = 0;
+  __syncthreads();
+  if (tid == 0) S.next = 0;
+  __syncthreads();
+  unsigned n_words = 0, n_cand = 0, n_ref = 0, n_ab = 0, n_units = 0, n_leaf = 0;
   for (;;) {
-    int c0 = 0;
-    if (lane == 0) c0 = atomicAdd(&S.next, R);
-    c0 = __shfl_sync(FULL, c0, 0);
-    if (c0 >= nc) break;
-    // lane 0 reads the (concurrently updated) threshold and broadcasts it: every lane must take
-    // the same branch below, since ed_warp_multi uses full-warp shuffles
-    float thr = 0.f, bsf = 0.f;
+    int u = 0;
+    float thr = 0.f;
     if (lane == 0) {
+      u = atomicAdd(&S.next, 1);
       thr = *(volatile float*)&S.thr;
-      bsf = *(volatile float*)&S.bsf;
     }
+    u = __shfl_sync(FULL, u, 0);
     thr = __shfl_sync(FULL, thr, 0);
-    bsf = __shfl_sync(FULL, bsf, 0);
-    const float* rows[R];
-    float2 st[R];
-    bool on[R];
-    int oidx[R];
-    bool any = false;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int c = c0 + r;
-      const unsigned long long e = c < nc ? s_cand[c] : ~0ull;
-      on[r] = c < nc && lb_of(e) <= thr;
-      oidx[r] = -1;
-      rows[r] = A.series;
-      st[r] = make_float2(0.f, 0.f);
-      if (on[r]) {
-        const uint32_t pos = (uint32_t)e;
-        oidx[r] = A.perm[pos];
-        st[r] = A.stats[pos];
-        rows[r] = A.series + (int64_t)oidx[r] * A.len;
-        any = true;
-      }
-    }
-    if (!any) {
-      if (sorted) break;  // every later candidate has a larger LB
+    if (u >= units) break;
+    const int e = u / ppl, part = u % ppl;
+    const unsigned long long ent = list[e];
+    if (lb_of(ent) > thr) {
+      if (sorted) break;  // every later leaf has a larger LB
       continue;
     }
-    float d2[R];
-    bool ab[R];
-    ed_warp_multi<NF, R>(rows, st, on, s_qh4, nf4, bsf, d2, ab);
-    ++n_waves;
-    if (lane == 0) {
+    ++n_units;
+    n_leaf += part == 0;
+    const int64_t base = (int64_t)(uint32_t)ent * B + (int64_t)part * span;
+    uint4 wr[WMAX][NC];
+    bool ok[WMAX];
+#pragma unroll
+    for (int i = 0; i < WMAX; ++i) {
+      const int64_t pos = base + i * 32 + lane;
+      ok[i] = i < wpl && pos < A.n;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) wr[i][c] = ok[i] ? ld_stream_u4(A.words + pos * A.WS + 16 * c) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    float lbv[WMAX];
+#pragma unroll
+    for (int i = 0; i < WMAX; ++i) {
+      lbv[i] = ok[i] ? word_lb<LT>(wr[i], s_T, thr) : __int_as_float(0x7fffffff);  // NaN: never <= thr
+      n_words += ok[i];
+      n_cand += lbv[i] <= thr;
+    }
+    for (;;) {  // refine this unit's candidates, R lowest LBs at a time
+      float bsf = 0.f;
+      if (lane == 0) {
+        thr = *(volatile float*)&S.thr;
+        bsf = *(volatile float*)&S.bsf;
+      }
+      thr = __shfl_sync(FULL, thr, 0);
+      bsf = __shfl_sync(FULL, bsf, 0);
+      const float* rows[R];
+      float2 st[R];
+      bool on[R];
+      int oidx[R];
+      bool any = false;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        if (!on[r]) continue;
-        ++n_ref;
-        if (ab[r]) {
-          ++n_ab;
-          continue;
+        unsigned long long best = ~0ull;
+#pragma unroll
+        for (int i = 0; i < WMAX; ++i)
+          if (lbv[i] <= thr) {
+            const unsigned long long key = pack(lbv[i], (uint32_t)(i * 32 + lane));
+            best = key < best ? key : best;
+          }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          const unsigned long long other = __shfl_xor_sync(FULL, best, o);
+          best = other < best ? other : best;
         }
-        const int n = *(volatile int*)&S.tkn;
-        const float kd = *(volatile float*)&s_tkd[n > 0 ? n - 1 : 0];
-        if (n < A.k || d2[r] <= kd) topk_insert(A, S, s_tkd, s_tki, d2[r], oidx[r]);
+        on[r] = best != ~0ull;
+        oidx[r] = -1;
+        rows[r] = A.series;
+        st[r] = make_float2(0.f, 0.f);
+        if (on[r]) {
+          const int slot = (int)(uint32_t)best;
+#pragma unroll
+          for (int i = 0; i < WMAX; ++i)
+            if (slot == i * 32 + lane) lbv[i] = __int_as_float(0x7fffffff);  // taken
+          const int64_t pos = base + slot;
+          oidx[r] = A.perm[pos];
+          st[r] = A.stats[pos];
+          rows[r] = A.series + (int64_t)oidx[r] * A.len;
+          any = true;
+        }
+      }
+      if (!any) break;
+      float d2[R];
+      bool ab[R];
+      ed_warp_multi<NF, R>(rows, st, on, s_qh4, nf4, bsf, d2, ab);
+      if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!on[r]) continue;
+          ++n_ref;
+          if (ab[r]) {
+            ++n_ab;
+            continue;
+          }
+          bool ins;
+          if (S.gslot >= 0) {
+            ins = d2[r] <= *(volatile float*)&S.bsf;
+          } else {
+            const int n = *(volatile int*)&S.tkn;
+            const float kd = *(volatile float*)&s_tkd[n > 0 ? n - 1 : 0];
+            ins = n < A.k || d2[r] <= kd;
+          }
+          if (ins) topk_insert(A, S, s_tkd, s_tki, d2[r], oidx[r]);
+        }
       }
     }
   }
+  n_cand = __reduce_add_sync(FULL, n_cand);
+  n_words = __reduce_add_sync(FULL, n_words);
   if (lane == 0) {
+    if (n_leaf) atomicAdd(&S.st[0], n_leaf);
+    if (n_words) atomicAdd(&S.st[1], n_words);
+    if (n_cand) atomicAdd(&S.st[2], n_cand);
     if (n_ref) atomicAdd(&S.st[3], n_ref);
     if (n_ab) atomicAdd(&S.st[4], n_ab);
-    if (n_waves) atomicAdd(&S.st[9], n_waves);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    S.ncand = 0;
-    S.next = 0;
+    if (n_units) atomicAdd(&S.st[8], n_units);
+    if (n_ref) atomicAdd(&S.st[9], (n_ref + R - 1) / R);
   }
   __syncthreads();
 }
 
-// scan the words of the listed blocks (a7) and refine (a8), batch by batch.  The words of batch
-// i+1 are loaded into registers before batch i's candidates are appended and refined, so their
-// HBM latency overlaps the refine (software pipelining over the batch loop).
-template <int LT, int NF>
-__device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long* list, int cnt, bool sorted,
-                            const float* s_T, unsigned long long* s_cand, float* s_tkd, int* s_tki, float* s_wd,
-                            int* s_wi, const float4* s_qh4) {
+// leaves per word batch, per scan task (8 batches) and the front's own budget (64 batches)
+template <int LT>
+__device__ __forceinline__ int batch_blocks(int B) {
+  constexpr int BW = LT == 16 ? CAP_C : (LT == 32 ? CAP_C / 2 : CAP_C / 4);
+  return B <= BW ? BW / B : 1;
+}
+template <int LT>
+__device__ __forceinline__ int chunk_blocks(int B) { return 8 * batch_blocks<LT>(B); }
+
+// front: append `n` leaf entries of query q to the pool as scan tasks of ranks S.ntask, S.ntask+1, ...
+template <int LT>
+__device__ void publish_tasks(const QArgs& A, QShared& S, int q, const unsigned long long* list, int n, bool sorted,
+                              bool dense_cand) {
+  if (n <= 0) return;
   const int tid = threadIdx.x;
-  const int B = A.B;
-  constexpr int BW = LT == 16 ? CAP_C : (LT == 32 ? CAP_C / 2 : CAP_C / 4);  // words per batch
-  const int G = B <= BW ? BW / B : 1;    // blocks per batch
-  const int SUB = B <= BW ? 1 : B / BW;  // batches per block
-  const int span = B <= BW ? B : BW;
-  const int nbatch = ((cnt + G - 1) / G) * SUB;
-  if (nbatch == 0) return;
-  constexpr int WPT = BW / kThreads;  // words per thread per batch
-  constexpr int NC = LT / 16;
-  int64_t pos[WPT];
-  bool valid[WPT];
-  uint4 wr[WPT][NC];
-  auto issue = [&](int bi, float thr) {
-    const int e0 = (bi / SUB) * G, sub = bi % SUB;
-#pragma unroll
-    for (int t = 0; t < WPT; ++t) {
-      const int w = tid + t * kThreads;
-      const int u = w / span, m = w % span;
-      const int e = e0 + u;
-      valid[t] = bi < nbatch && e < cnt && u < G;
-      pos[t] = 0;
-      if (valid[t]) {
-        const unsigned long long ent = list[e];
-        pos[t] = (int64_t)(uint32_t)ent * B + (int64_t)sub * BW + m;
-        valid[t] = lb_of(ent) <= thr && pos[t] < A.n;
-      }
-#pragma unroll
-      for (int c = 0; c < NC; ++c)
-        wr[t][c] = valid[t] ? ld_stream_u4(A.words + pos[t] * A.WS + 16 * c) : make_uint4(0u, 0u, 0u, 0u);
-    }
-  };
-  issue(0, S.thr);
-  for (int bi = 0; bi < nbatch; ++bi) {
-    const float thr = S.thr;
-    const int e0 = (bi / SUB) * G, sub = bi % SUB;
-    if (sorted && lb_of(list[e0]) > thr) return;  // every later block has a larger LB
-    if (tid == 0) S.st[8] += 1;
-    if (tid == 0 && sub == 0) {
-      unsigned int surv = 0;
-      for (int u = 0; u < G && e0 + u < cnt; ++u) surv += lb_of(list[e0 + u]) <= thr;
-      S.st[0] += surv;
-    }
-    float lbs[WPT];
-    bool vcur[WPT];
-    int64_t pcur[WPT];
-    unsigned int scanned = 0;
-#pragma unroll
-    for (int t = 0; t < WPT; ++t) {
-      vcur[t] = valid[t];
-      pcur[t] = pos[t];
-      lbs[t] = valid[t] ? word_lb<LT>(wr[t], s_T, thr) : INFINITY;
-      scanned += valid[t];
-    }
-    issue(bi + 1, thr);  // next batch's loads fly during this batch's append + refine
-#pragma unroll
-    for (int t = 0; t < WPT; ++t)
-      warp_append(vcur[t] && lbs[t] <= thr, pack(lbs[t], (uint32_t)pcur[t]), s_cand, &S.ncand);
-    scanned = __reduce_add_sync(FULL, scanned);
-    if ((tid & 31) == 0 && scanned) atomicAdd(&S.st[1], scanned);
-    __syncthreads();
-    if (tid == 0) S.st[2] += S.ncand;
-    refine_candidates<LT, NF>(A, S, s_cand, s_tkd, s_tki, s_qh4);
+  const int CH = chunk_blocks<LT>(A.B);
+  const int nt = (n + CH - 1) / CH;
+  const int set = dense_cand ? 1 : 0;
+  if (tid == 0) {
+    S.off = (long long)atomicAdd(A.pool_used, (unsigned long long)n);
+    S.chunk = S.ntask;
+    S.ntask += nt;
+    atomicMax(&A.counters[2 * set], S.ntask);
   }
+  __syncthreads();
+  const int64_t off = S.off;
+  const int r0 = S.chunk;
+  for (int i = tid; i < n; i += kThreads) A.pool[off + i] = list[i];
+  const int flags = sorted ? kTaskSorted : 0;
+  ScanTask* tasks = A.tasks + (int64_t)set * A.rank_cap * A.q;
+  int* rc = A.rank_count + set * A.rank_cap;
+  for (int i = tid; i < nt; i += kThreads) {
+    ScanTask t;
+    t.off = off + (int64_t)i * CH;
+    t.q = q;
+    t.cnt_flags = (n - i * CH < CH ? n - i * CH : CH) | flags | (dense_cand ? kTaskDense : 0);
+    const int r = r0 + i;
+    t.rank = r;
+    if (r < A.rank_cap) tasks[(int64_t)r * A.q + atomicAdd(&rc[r], 1)] = t;
+  }
+  __syncthreads();
+}
+
+// scan mode: all CTAs pull tasks until the pool is drained; rank-major order (every query's lowest-
+// LB chunk first), so a query's later chunks usually meet its final BSF and are rejected unread
+template <int LT, int NF>
+__device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, unsigned long long* s_cand, float* s_tkd, int* s_tki,
+                           float* s_wd, int* s_wi, float4* s_qh4) {
+  const int tid = threadIdx.x;
+  bool dense_go = false;
+  if (A.qd_counter) {
+    const int qd = *A.qd_counter;
+    const unsigned long long est = *reinterpret_cast<const unsigned long long*>(A.qd_counter + 6);
+    dense_go = qd > 0 && est >= (unsigned long long)A.dense_rows;
+  }
+  const int nsets = dense_go ? 1 : 2;
+  __shared__ ScanTask s_task;
+  __shared__ int s_have;
+  if (tid == 0) {
+    for (int i = 0; i < 10; ++i) S.st[i] = 0;
+    S.gslot = -1;
+  }
+  int cur = -1;
+  for (;;) {
+    if (tid == 0) {
+      int have = 0;
+      for (int set = 0; set < nsets && !have; ++set) {
+        const int ranks = A.counters[2 * set] < A.rank_cap ? A.counters[2 * set] : A.rank_cap;
+        unsigned* cursor = reinterpret_cast<unsigned*>(&A.counters[2 * set + 1]);
+        const int* rc = A.rank_count + set * A.rank_cap;
+        for (;;) {  // rank-major cursor over tasks[r * q + i], jumping over each bucket's empty tail
+          const unsigned t = atomicAdd(cursor, 1u);
+          const int r = (int)(t / (unsigned)A.q), i = (int)(t % (unsigned)A.q);
+          if (r >= ranks) break;
+          if (i < rc[r]) {
+            s_task = A.tasks[(int64_t)set * A.rank_cap * A.q + t];
+            have = 1;
+            break;
+          }
+          atomicMax(cursor, (unsigned)(r + 1) * (unsigned)A.q);
+        }
+      }
+      s_have = have;
+      if (have) {  // quick reject: a sorted chunk whose first leaf's LB is above the query's BSF
+        volatile QState* h = &A.qs[s_task.q];
+        // a dense candidate reached the scan with only its take-round BSF: let its lowest-LB chunk
+        // (rank 0, dispatched before any other rank) tighten the BSF before the others start
+        if ((s_task.cnt_flags & kTaskDense) && s_task.rank > 0)
+          while (h->done < 1) __nanosleep(500);
+        const float thr = thr_of(h->bsf);
+        S.take = (s_task.cnt_flags & kTaskSorted) && lb_of(A.pool[s_task.off]) > thr;
+      }
+    }
+    __syncthreads();
+    if (!s_have) break;
+    const ScanTask tk = s_task;
+    const int q = tk.q;
+    volatile QState* h = &A.qs[q];
+    if (!S.take) {
+      if (q != cur) {
+        const float4* T4 = reinterpret_cast<const float4*>(A.q_T + (int64_t)q * LT * 256);
+        for (int i = tid; i < LT * 64; i += kThreads) reinterpret_cast<float4*>(s_T)[i] = T4[i];
+        for (int i = tid; i < A.len; i += kThreads) reinterpret_cast<float*>(s_qh4)[i] = A.q_hat[(int64_t)q * A.len + i];
+        cur = q;
+      }
+      if (tid == 0) {
+        S.gslot = q;
+        S.bsf_init = h->bsf_init;
+        S.bsf = h->bsf;
+        S.thr = thr_of(S.bsf);
+        S.ncand = 0;
+        S.next = 0;
+        S.lock = 0;
+      }
+      __syncthreads();
+      scan_blocks<LT, NF>(A, S, A.pool + tk.off, tk.cnt_flags & kTaskCnt, (tk.cnt_flags & kTaskSorted) != 0, s_T,
+                          s_tkd, s_tki, s_qh4);
+      __syncthreads();
+    }
+    if (tid == 0) {
+      __threadfence();
+      S.take = atomicAdd(const_cast<int*>(&h->done), 1) == h->ntasks - 1;
+      if (S.take) __threadfence();
+      S.gslot = -1;
+    }
+    __syncthreads();
+    if (S.take) {  // last task of this query: write its result
+      const int n = h->tkn;
+      for (int r = tid; r < A.k; r += kThreads) {
+        const bool ok = r < n;
+        A.od[(int64_t)q * A.k + r] = ok ? sqrtf(h->tkd[r]) : INFINITY;
+        A.oi[(int64_t)q * A.k + r] = ok ? A.goff + h->tki[r] : -1;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && A.dstats)
+    for (int i = 0; i < 10; ++i)
+      if (S.st[i]) atomicAdd(&A.dstats[2 + i], (unsigned long long)S.st[i]);
 }
 
 // envelope LB of a node (leaf LB): sum_j Tlo[j][min_j] + Thi[j][max_j]
@@ -437,7 +599,7 @@ __device__ void env_level(const QArgs& A, int L, const unsigned long long* paren
 // the shared-memory list `take` (up to CAP_B of them), the rest to `rem`.  4 entries per thread
 // per iteration with all loads issued first.
 __device__ void filter_list(const unsigned long long* src, int cnt, float thr, float tau, unsigned long long* take,
-                            int* ntake, unsigned long long* rem, int* nrem) {
+                            int* ntake, unsigned long long* rem, int* nrem, int cap = CAP_B) {
   constexpr int U = 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int ee = warp * 32 * U; ee < cnt; ee += kThreads * U) {
@@ -461,7 +623,7 @@ __device__ void filter_list(const unsigned long long* src, int cnt, float thr, f
         base = __shfl_sync(FULL, base, leader);
       }
       const int slot = base + __popc(m & ((1u << lane) - 1u));
-      const bool got = tk && slot < CAP_B;
+      const bool got = tk && slot < cap;
       if (got) take[slot] = ent[u];
       warp_append(keep && !got, ent[u], rem, nrem);
     }
@@ -469,7 +631,7 @@ __device__ void filter_list(const unsigned long long* src, int cnt, float thr, f
 }
 
 template <int LT, int NF>
-__global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
+__global__ void __launch_bounds__(kThreads, 2) k_query(const __grid_constant__ QArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ QShared S;
   constexpr int UB0 = 2 * LT * 256 * 4, UB1 = CAP_B * 8, UB2 = NF * 128 * 8;
@@ -483,18 +645,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
   double* s_qd = reinterpret_cast<double*>(s_u);
   unsigned long long* s_blist = reinterpret_cast<unsigned long long*>(s_u);
   unsigned long long* s_cand = reinterpret_cast<unsigned long long*>(s_u + UB);
-  float* s_tkd = reinterpret_cast<float*>(s_cand + CAP_C);
+  float* s_tkd = reinterpret_cast<float*>(s_cand + CAPC);
   int* s_tki = reinterpret_cast<int*>(s_tkd + KMAX);
   float* s_wd = reinterpret_cast<float*>(s_tki + KMAX);
   int* s_wi = reinterpret_cast<int*>(s_wd + 8);
   __shared__ uint8_t s_qw[SOFA_MAX_L];
   __shared__ unsigned long long s_seed;
+  __shared__ int s_dense;
+  __shared__ long long s_dec[4];  // dense decision inputs: flagged, leaves after take, pass, words
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int len = A.len, nf4 = len >> 2, l = A.l, a = A.a;
   unsigned long long* gl = A.gscratch + (int64_t)blockIdx.x * 2 * A.nb;
   unsigned long long* gl2 = gl + A.nb;
 
+  if (A.mode == 1) {
+    scan_tasks<LT, NF>(A, S, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+    return;
+  }
   for (;;) {
     if (tid == 0) S.qi = atomicAdd(A.qcounter, 1);
     __syncthreads();
@@ -537,6 +705,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
         S.tkn = 0;
         S.next = 0;
         S.lock = 0;
+        S.gslot = -1;
         for (int i = 0; i < 10; ++i) S.st[i] = 0;
         const float bi = A.bsf_init ? A.bsf_init[qi] : INFINITY;
         S.bsf_init = bi;
@@ -592,7 +761,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
     t_phase[1] = clock64();
     if (tid == 0) s_seed = pack(0.f, (uint32_t)b0);
     __syncthreads();
-    scan_blocks<LT, NF>(A, S, &s_seed, A.nb > 0 ? 1 : 0, true, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+    scan_blocks<LT, NF>(A, S, &s_seed, A.nb > 0 ? 1 : 0, true, s_T, s_tkd, s_tki, s_qh4);
     t_phase[2] = clock64();
     // ---------------------------------------------------------------- a6: envelope tree descent
     // top level: every node; lower levels: the kFan children of each surviving parent
@@ -629,13 +798,128 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
     // sorted and scanned first — that tightens the BSF to (nearly) its final value — and the rest
     // is re-filtered against it and scanned in storage order (LB re-checked per block).
     {
-      const int cnt = S.cnt;
+      int cnt = S.cnt;
       if (tid == 0) S.st[6] += cnt;
+      if (tid == 0) {
+        s_dense = -1;
+        s_dec[0] = s_dec[1] = s_dec[2] = s_dec[3] = 0;
+      }
+      __syncthreads();  // every thread must see -1 before the (uniform) branch below
+      if (A.dense_min > 0 && cnt >= A.dense_min) {
+        // f1 decision: refine the TAKE0 lowest-LB leaves first (tightens the BSF, as MESSI's first
+        // DeleteMin rounds do), re-filter the rest against it; if >= dense_min leaves still survive,
+        // the SFA bound cannot prune this query and it goes to the batched dense path.
+        constexpr int TAKE0 = 8;
+        s_cand[tid] = gl[((int64_t)tid * cnt) / kThreads];
+        if (tid == 0) {
+          S.take = 0;
+          S.rem = 0;
+        }
+        __syncthreads();
+        bitonic_sort_u64(s_cand, kThreads);
+        int r = (int)(((int64_t)kThreads * TAKE0) / cnt);
+        r = r < 0 ? 0 : (r > kThreads - 1 ? kThreads - 1 : r);
+        const float tau = lb_of(s_cand[r]);
+        filter_list(gl, cnt, S.thr, tau, s_blist, &S.take, gl2, &S.rem, TAKE0);
+        __syncthreads();
+        const int ntake = S.take < TAKE0 ? S.take : TAKE0;
+        const int nrem = S.rem;
+        bitonic_sort_u64(s_blist, ntake);
+        scan_blocks<LT, NF>(A, S, s_blist, ntake, true, s_T, s_tkd, s_tki, s_qh4);
+        if (tid == 0) {
+          S.take = 0;
+          S.rem = 0;
+        }
+        __syncthreads();
+        filter_list(gl2, nrem, S.thr, -1.f, s_blist, &S.take, gl, &S.rem);
+        __syncthreads();
+        cnt = S.rem;
+        // power of the SFA bound on this query: the fraction of the take blocks' words whose LB is
+        // still <= the tightened threshold (high-frequency data ~1, noisy members ~1e-3).  Dense only
+        // if many leaves survive AND most of their words would have to be refined anyway.
+        int pass = 0;
+        if (cnt >= A.dense_min) {
+          const float thr = S.thr;
+          const int nw = ntake * A.B < 2048 ? ntake * A.B : 2048;
+          for (int w = tid; w < nw; w += kThreads) {
+            const int64_t pos = (int64_t)(uint32_t)s_blist[w / A.B] * A.B + (w % A.B);
+            if (pos < A.n) {
+              uint4 wr[LT / 16];
+#pragma unroll
+              for (int c = 0; c < LT / 16; ++c) wr[c] = ld_stream_u4(A.words + pos * A.WS + 16 * c);
+              pass += word_lb<LT>(wr, s_T, thr) <= thr;
+            }
+          }
+          pass = __reduce_add_sync(FULL, pass);
+          if (lane == 0) atomicAdd(&S.take, pass);
+          __syncthreads();
+          // estimated sparse refines of this query: surviving leaves x B x word pass rate
+          const double est = (double)cnt * A.B * S.take / (nw > 0 ? nw : 1);
+          if (tid == 0) {
+            s_dec[1] = cnt;
+            s_dec[2] = S.take;
+            s_dec[3] = nw;
+          }
+          if (tid == 0 && (A.dense_force || est * 32.0 >= (double)A.n)) {
+            s_dense = atomicAdd(A.qd_counter, 1);
+            s_dec[0] = 1;
+            atomicAdd(reinterpret_cast<unsigned long long*>(A.qd_counter + 6),
+                      A.dense_force ? (unsigned long long)A.dense_rows : (unsigned long long)est);
+          }
+        }
+        __syncthreads();
+      }
+      if (s_dense >= 0) {
+        // publish the query's state to its dense slot; dense.cu finishes it
+        const int slot = s_dense;
+        for (int t = tid; t < len; t += kThreads) A.d_qhat[(int64_t)slot * len + t] = reinterpret_cast<const float*>(s_qh4)[t];
+        for (int r = tid; r < S.tkn; r += kThreads) {
+          A.d_tkd[(int64_t)slot * A.k + r] = s_tkd[r];
+          A.d_tki[(int64_t)slot * A.k + r] = s_tki[r];
+        }
+        if (warp == 0) {
+          double nq = 0.0, sq = 0.0;
+          for (int t = lane; t < len; t += 32) {
+            const double v = reinterpret_cast<const float*>(s_qh4)[t];
+            nq += v * v;
+            sq += v;
+          }
+          nq = warp_sum_f64(nq);
+          sq = warp_sum_f64(sq);
+          if (lane == 0) {
+            // TF32 operands keep 10 mantissa bits: |dot error| <= gamma sum|q x|, gamma = 2^-9 (two
+            // truncated operands) + len 2^-22 (fp32 accumulation, doubled for safety), +5%
+            const double gamma = 1.05 * 0x1p-9 + (double)len * 0x1p-22;
+            A.d_qparams[slot] = make_float4((float)nq, (float)sq, (float)(2.0 * gamma * sqrt(nq) * 1.0001),
+                                            (float)(2e-4 * nq + 1e-3));
+            A.d_qidx[slot] = qi;
+            A.d_binit[slot] = S.bsf_init;
+            A.d_bsf[slot] = S.bsf;
+            A.d_thr[slot] = S.bsf;
+            A.d_tkn[slot] = S.tkn;
+            A.d_lock[slot] = 0;
+            A.d_overflow[slot] = 0;
+          }
+        }
+      }
+      // the remaining leaves, in ascending LB (MESSI's priority-queue order): up to
+      // `budget` of them are scanned here with the stop rule; what a heavy query has left beyond that
+      // becomes scan tasks spread over all CTAs.  A dense candidate's leaves are only published
+      // (scanned only if the batch decides against the dense pass).
+      const bool dc = s_dense >= 0;
+      const int CH = chunk_blocks<LT>(A.B);
+      const int budget = A.front_batches * batch_blocks<LT>(A.B);  // leaves the front scans itself
+      if (tid == 0) S.ntask = 0;
       if (cnt <= CAP_B) {
         for (int i = tid; i < cnt; i += kThreads) s_blist[i] = gl[i];
         __syncthreads();
         bitonic_sort_u64(s_blist, cnt);
-        scan_blocks<LT, NF>(A, S, s_blist, cnt, true, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+        int nloc = dc ? 0 : (cnt < budget ? cnt : budget);
+        if (!dc && cnt - nloc <= CH) nloc = cnt;  // short remainder: finish it here
+        if (nloc) scan_blocks<LT, NF>(A, S, s_blist, nloc, true, s_T, s_tkd, s_tki, s_qh4);
+        int rest = cnt - nloc;
+        if (!dc && rest > 0 && lb_of(s_blist[nloc]) > S.thr) rest = 0;  // stop rule: nothing left below the BSF
+        publish_tasks<LT>(A, S, qi, s_blist + nloc, rest, true, dc);
       } else {
         if (tid == 0) S.st[7] += 1;
         s_cand[tid] = gl[((int64_t)tid * cnt) / kThreads];
@@ -653,7 +937,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
         const int ntake = S.take < CAP_B ? S.take : CAP_B;
         const int nrem = S.rem;
         bitonic_sort_u64(s_blist, ntake);
-        scan_blocks<LT, NF>(A, S, s_blist, ntake, true, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+        const int nloc = dc ? 0 : (ntake < budget ? ntake : budget);
+        if (nloc) scan_blocks<LT, NF>(A, S, s_blist, nloc, true, s_T, s_tkd, s_tki, s_qh4);
+        int rest = ntake - nloc;
+        if (!dc && rest > 0 && lb_of(s_blist[nloc]) > S.thr) rest = 0;
+        publish_tasks<LT>(A, S, qi, s_blist + nloc, rest, true, dc);
         if (nrem > 0) {
           if (tid == 0) {
             S.take = 0;
@@ -662,20 +950,34 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
           __syncthreads();
           filter_list(gl2, nrem, S.thr, -1.f, s_blist, &S.take, gl, &S.rem);
           __syncthreads();
-          const int n2 = S.rem;
-          if (n2 <= CAP_B) {
-            for (int i = tid; i < n2; i += kThreads) s_blist[i] = gl[i];
-            __syncthreads();
-            bitonic_sort_u64(s_blist, n2);
-            scan_blocks<LT, NF>(A, S, s_blist, n2, true, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
-          } else {
-            scan_blocks<LT, NF>(A, S, gl, n2, false, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
-          }
+          publish_tasks<LT>(A, S, qi, gl, S.rem, false, dc);
+        }
+      }
+      __syncthreads();
+      if (S.ntask > 0) {  // hand the query's state to the scan CTAs
+        QState* h = &A.qs[qi];
+        if (tid == 0 && A.dstats) {
+          atomicAdd(&A.dstats[22], (unsigned long long)S.ntask);
+          atomicAdd(&A.dstats[23], 1ull);
+        }
+        for (int i = tid; i < LT * 256; i += kThreads) A.q_T[(int64_t)qi * LT * 256 + i] = s_T[i];
+        for (int i = tid; i < len; i += kThreads) A.q_hat[(int64_t)qi * len + i] = reinterpret_cast<const float*>(s_qh4)[i];
+        for (int r = tid; r < S.tkn; r += kThreads) {
+          h->tkd[r] = s_tkd[r];
+          h->tki[r] = s_tki[r];
+        }
+        if (tid == 0) {
+          h->tkn = S.tkn;
+          h->lock = 0;
+          h->ntasks = S.ntask;
+          h->done = 0;
+          h->bsf = S.bsf;
+          h->bsf_init = S.bsf_init;
         }
       }
     }
     // ---------------------------------------------------------------- output
-    for (int r = tid; r < A.k; r += kThreads) {
+    for (int r = tid; s_dense < 0 && S.ntask == 0 && r < A.k; r += kThreads) {
       const bool ok = r < S.tkn;
       A.od[(int64_t)qi * A.k + r] = ok ? sqrtf(s_tkd[r]) : INFINITY;
       A.oi[(int64_t)qi * A.k + r] = ok ? A.goff + s_tki[r] : -1;
@@ -695,6 +997,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const QArgs A) {
       for (int i = 0; i < 4; ++i) tr[i] = t_phase[i + 1] - t_phase[i];
       for (int i = 0; i < 10; ++i) tr[4 + i] = S.st[i];
       tr[14] = blockIdx.x;
+      for (int i = 0; i < 4; ++i) tr[16 + i] = s_dec[i];
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       tr[15] = smid;
@@ -708,15 +1011,15 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
   QArgs A = A0;
   constexpr int UB0 = 2 * LT * 256 * 4, UB1 = CAP_B * 8, UB2 = NF * 128 * 8;
   constexpr int UB = UB0 > UB1 ? (UB0 > UB2 ? UB0 : UB2) : (UB1 > UB2 ? UB1 : UB2);
-  const size_t smem = NF * 128 * 4 + LT * 8 + LT * 256 * 4 + UB + CAP_C * 8 + KMAX * 8 + 8 * 8;
+  const size_t smem = NF * 128 * 4 + LT * 8 + LT * 256 * 4 + UB + CAPC * 8 + KMAX * 8 + 8 * 8;
   auto kern = k_query<LT, NF>;
   SOFA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0, sms = 148;
   SOFA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
   if (per_sm < 1) per_sm = 1;
-  int grid = sms * per_sm;
-  if (grid > A.q) grid = A.q;
+  // the whole GPU even for a small batch: CTAs without a query of their own help heavy ones
+  const int grid = sms * per_sm;
   const int64_t need = (int64_t)grid * 2 * (ix->nb > 0 ? ix->nb : 1);
   if (ix->gscratch_ctas < need) {
     if (ix->gscratch) cudaFree(ix->gscratch);
@@ -725,15 +1028,53 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
     ix->gscratch_ctas = need;
   }
   A.gscratch = ix->gscratch;
-  SOFA_CK(cudaMemsetAsync(ix->qcounter, 0, sizeof(int), st));
+  // qcounter ints: [0] query queue, [2..3] leaf pool entries used (u64), [4..7] scan counters
+  A.pool_used = reinterpret_cast<unsigned long long*>(ix->qcounter + 2);
+  A.counters = ix->qcounter + 4;
+  if (A.mode == 0) {
+    const int BW = LT == 16 ? CAP_C : (LT == 32 ? CAP_C / 2 : CAP_C / 4);
+    const int CH = 8 * (ix->B <= BW ? BW / ix->B : 1);
+    const int64_t qn = A.q, nb = ix->nb > 0 ? ix->nb : 1;
+    const int64_t ranks = (nb + CH - 1) / CH + 2;  // chunks one query can publish
+    const int64_t pool_need = qn * nb, task_need = qn * ranks;
+    if (ix->scan_q_cap != qn || ix->scan_LT != LT || ix->pool_cap < pool_need || ix->task_cap < task_need) {
+      void* old[] = {ix->qstate, ix->q_T, ix->q_hat, ix->pool, ix->tasks, ix->rank_count};
+      for (void* o : old)
+        if (o) cudaFree(o);
+      ix->qstate = ix->q_T = ix->q_hat = ix->pool = ix->tasks = ix->rank_count = nullptr;
+      SOFA_CK(cudaMalloc(&ix->qstate, (size_t)qn * sizeof(QState)));
+      SOFA_CK(cudaMalloc(&ix->q_T, (size_t)qn * LT * 256 * 4));
+      SOFA_CK(cudaMalloc(&ix->q_hat, (size_t)qn * SOFA_MAX_LEN * 4));
+      SOFA_CK(cudaMalloc(&ix->pool, (size_t)pool_need * 8));
+      SOFA_CK(cudaMalloc(&ix->tasks, (size_t)2 * task_need * sizeof(ScanTask)));
+      SOFA_CK(cudaMalloc(&ix->rank_count, (size_t)2 * ranks * 4));
+      ix->scan_q_cap = qn;
+      ix->scan_LT = LT;
+      ix->pool_cap = pool_need;
+      ix->task_cap = task_need;
+      ix->rank_cap = ranks;
+    }
+    SOFA_CK(cudaMemsetAsync(ix->qcounter, 0, 16 * sizeof(int), st));
+    SOFA_CK(cudaMemsetAsync(ix->rank_count, 0, (size_t)2 * ix->rank_cap * 4, st));
+  }
+  A.rank_count = reinterpret_cast<int*>(ix->rank_count);
+  A.rank_cap = (int)ix->rank_cap;
+  A.qs = reinterpret_cast<QState*>(ix->qstate);
+  A.q_T = reinterpret_cast<float*>(ix->q_T);
+  A.q_hat = reinterpret_cast<float*>(ix->q_hat);
+  A.pool = reinterpret_cast<unsigned long long*>(ix->pool);
+  A.tasks = reinterpret_cast<ScanTask*>(ix->tasks);
   kern<<<grid, kThreads, smem, st>>>(A);
   SOFA_LAUNCHED();
   return SOFA_OK;
 }
 
 int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
-                 cudaStream_t st) {
+                 cudaStream_t st, bool scan) {
   QArgs A{};
+  A.mode = scan ? 1 : 0;
+  A.front_batches = 64;
+  if (const char* e = getenv("SOFA_FRONT_BATCHES")) A.front_batches = atoi(e) > 0 ? atoi(e) : 1;  // tuning knob
   A.series = ix->series;
   A.n = ix->n;
   A.nb = ix->nb;
@@ -764,6 +1105,25 @@ int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_
   A.qcounter = ix->qcounter;
   A.dstats = ix->dstats;
   A.trace = ix->trace_on ? ix->trace : nullptr;
+  if (ix->dense_permille > 0 && ix->dense.q_cap >= q) {
+    const DenseScratch& D = ix->dense;
+    A.dense_min = (ix->nb * (ix->dense_permille < 1000 ? ix->dense_permille : 0) + 999) / 1000;
+    if (A.dense_min < 1) A.dense_min = 1;
+    A.dense_rows = dense_batch_rows(ix);
+    A.dense_force = ix->dense_permille >= 1000;
+    A.qd_counter = D.counters;
+    A.d_qhat = D.qhat;
+    A.d_qparams = D.qparams;
+    A.d_qidx = D.qidx;
+    A.d_binit = D.binit;
+    A.d_bsf = D.bsf;
+    A.d_thr = D.thr;
+    A.d_tkd = D.tkd;
+    A.d_tki = D.tki;
+    A.d_tkn = D.tkn;
+    A.d_lock = D.lock;
+    A.d_overflow = D.overflow;
+  }
   for (int j = 0; j < SOFA_MAX_L; ++j) A.weights[j] = j < ix->l ? (float)ix->model.weights[j] : 0.f;
   const int nf4 = ix->len / 4;
   const int NF = nf4 <= 32 ? 1 : nf4 <= 64 ? 2 : nf4 <= 128 ? 4 : 8;

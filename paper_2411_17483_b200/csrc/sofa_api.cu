@@ -152,7 +152,8 @@ int sofa_learn_model(const float* sample_dev, int64_t S, int32_t len, int32_t l,
 
 void sofa_free(sofa_index* ix) {
   if (!ix) return;
-  void* bufs[] = {ix->words, ix->stats, ix->perm, ix->env, ix->bkey, ix->basis32, ix->basis64, ix->edges32,
+  free_dense_scratch(ix);
+  void* bufs[] = {ix->qstate, ix->q_T, ix->q_hat, ix->pool, ix->tasks, ix->rank_count, ix->words, ix->stats, ix->stats_orig, ix->perm, ix->env, ix->bkey, ix->basis32, ix->basis64, ix->edges32,
                   ix->edges64, ix->gscratch, ix->qcounter, ix->dstats, ix->hq_dev, ix->hd_dev, ix->hi_dev,
                   ix->trace};
   for (void* p : bufs)
@@ -189,6 +190,7 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
   ix->global_offset = opts.global_offset;
   ix->global_n = gn;
   ix->series = series_dev;
+  ix->dense_permille = opts.dense_permille == 0 ? 100 : (opts.dense_permille < 0 ? 0 : opts.dense_permille);
   cudaGetDevice(&ix->device);
   auto bail = [&](int code) {
     sofa_free(ix);
@@ -239,7 +241,7 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
   int32_t* iota = nullptr;
   void* tmp = nullptr;
   auto freeall = [&]() {
-    void* ps[] = {words_u, stats_u, keys_u, keys_s, iota, tmp};
+    void* ps[] = {words_u, keys_u, keys_s, iota, tmp};
     for (void* p : ps)
       if (p) cudaFree(p);
   };
@@ -254,6 +256,7 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
   } while (0)
   BCK(cudaMalloc(&words_u, (size_t)n * WS));
   BCK(cudaMalloc(&stats_u, (size_t)n * 8));
+  ix->stats_orig = stats_u;  // (mu, 1/sigma) in original row order, kept for the dense path
   BCK(cudaMalloc(&keys_u, (size_t)n * 8));
   BCK(cudaMalloc(&keys_s, (size_t)n * 8));
   BCK(cudaMalloc(&iota, (size_t)n * 4));
@@ -321,10 +324,21 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
   }
   if (stats) ix->trace_q = q;
   int rc;
-  if (ix->n == 0)
+  const bool dense = ix->n > 0 && ix->dense_permille > 0;
+  if (dense) {
+    if ((rc = ensure_dense_scratch(ix, q, k))) return rc;
+    SOFA_CK(cudaMemsetAsync(ix->dense.counters, 0, 64, st));
+  }
+  if (ix->n == 0) {
     rc = launch_fill_pad(out_dist_dev, out_idx_dev, (int64_t)q * k, st);
-  else
-    rc = launch_query(ix, queries_dev, q, k, bsf_init_dev, out_dist_dev, out_idx_dev, st);
+  } else {
+    // front (per query) -> dense pass for flagged queries if the batch warrants it -> scan tasks
+    // (every other leaf chunk of every query, spread over all CTAs); the dense and scan kernels read
+    // the batch decision from device counters, so there is no host synchronisation in between
+    rc = launch_query(ix, queries_dev, q, k, bsf_init_dev, out_dist_dev, out_idx_dev, st, false);
+    if (!rc && dense) rc = launch_dense(ix, q, k, out_dist_dev, out_idx_dev, stats != nullptr, st);
+    if (!rc) rc = launch_query(ix, queries_dev, q, k, bsf_init_dev, out_dist_dev, out_idx_dev, st, true);
+  }
   if (rc) return rc;
   if (stats) {
     unsigned long long h[32] = {};
@@ -346,6 +360,11 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
     stats->max_query_cycles = (int64_t)h[16];
     stats->max_list_blocks = (int64_t)h[17];
     stats->max_batches = (int64_t)h[18];
+    stats->dense_queries = (int64_t)h[19];
+    stats->dense_candidates = (int64_t)h[20];
+    stats->dense_refined = (int64_t)h[21];
+    stats->scan_tasks = (int64_t)h[22];
+    stats->scan_queries = (int64_t)h[23];
   }
   return SOFA_OK;
 }

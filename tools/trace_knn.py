@@ -34,3 +34,9 @@ src = datagen.query_sources(w) if w.query_kind == "noisy" else None
 if src is not None:
     print("slowest queries found source:", [(int(r), int(i[r, 0]), int(src[r])) for r in order[:12]])
     print("dist of slowest:", d[order[:12], 0].cpu().numpy())
+fl = np.nonzero(tr[:, 16] > 0)[0]
+print("dense-flagged queries:", len(fl))
+cand = np.nonzero(tr[:, 17] > 0)[0]
+print("queries that reached the dense decision:", len(cand))
+for r in cand[np.argsort(-tr[cand, 17])][:20]:
+    print(r, "leaves", tr[r, 17], "pass", tr[r, 18], "/", tr[r, 19], "flag", tr[r, 16], "cycles", tr[r, :4].sum())
