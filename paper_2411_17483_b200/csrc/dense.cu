@@ -40,7 +40,7 @@ constexpr int DSTAGES = 4;              // TMA -> MMA pipeline depth
 constexpr int DA_BYTES = DM * DKC * 4;  // 16 KB
 constexpr int DB_BYTES = DN * DKC * 4;  // 32 KB
 constexpr int D_THREADS = 320;          // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2..9 epilogue
-constexpr int D_UBK = 32;               // k-th-smallest UB tracking for k <= 32 (else exact BSF only)
+constexpr int D_UBK = SOFA_MAX_K;       // k-th-smallest UB tracking (local memory; updates are rare)
 constexpr size_t D_SMEM = 1024 + DSTAGES * (DA_BYTES + DB_BYTES) + 2 * DN * 8 + 64 + 256;
 
 // ------------------------------------------------------------------------------- PTX helpers
@@ -154,6 +154,24 @@ __device__ __noinline__ void ub_insert(float* ubl, int& nub, float& ubk, int kk,
   if (nub == kk) ubk = ubl[kk - 1];
 }
 
+// The j-th item (query tile m, series tile t) of this CTA.  When the grid holds at least one CTA
+// per query tile, CTA b serves tile m = b % mt only (so per-query state persists across its items)
+// and the CTAs sharing a series tile t run together (its rows are read from HBM once, then L2).
+__device__ __forceinline__ bool dense_item(int64_t j, int64_t mt, int64_t n_tiles, int& m, int64_t& t) {
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  if (mt <= G) {
+    const int64_t per = G / mt;
+    if (b >= per * mt) return false;
+    m = (int)(b % mt);
+    t = b / mt + j * per;
+    return t < n_tiles;
+  }
+  const int64_t it = b + j * G;
+  m = (int)(it % mt);
+  t = it / mt;
+  return t < n_tiles;
+}
+
 template <bool KONE>
 __global__ void __launch_bounds__(D_THREADS, 1)
     k_dense_screen(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX, const DenseArgs A) {
@@ -175,7 +193,6 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     return;  // batch decision: sparse (the deferred k_query launch finishes the flagged queries)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t mt = (qd + DM - 1) / DM;
-  const int64_t items = mt * A.n_tiles;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < DSTAGES; ++s) {
@@ -206,9 +223,9 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int m = (int)(it % mt);
-        const int64_t t = it / mt;
+      int m;
+      int64_t t;
+      for (int64_t j = 0; dense_item(j, mt, A.n_tiles, m, t); ++j) {
         for (int kc = 0; kc < A.KC; ++kc) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], DA_BYTES + DB_BYTES);
@@ -226,8 +243,9 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      int64_t local = 0;
-      for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ++local) {
+      int m;
+      int64_t t, local = 0;
+      for (int64_t j = 0; dense_item(j, mt, A.n_tiles, m, t); ++j, ++local) {
         const int acc = (int)(local & 1);
         const uint32_t aph = (uint32_t)((local >> 1) & 1);
         mbar_wait(&tempty[acc], aph ^ 1);
@@ -262,10 +280,21 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     const int row = eq * 32 + lane;
     const int et = (warp - 2) * 32 + lane;  // 0..255: one series of the tile each in the fill
     const float nlen = (float)A.len;
-    int64_t local = 0;
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ++local) {
-      const int m = (int)(it % mt);
-      const int64_t t = it / mt;
+    // per thread (one query row): the k smallest UB_g it has seen, kept across all of the CTA's items
+    // (the grid is a multiple of the number of query tiles, so a CTA always serves the same tile)
+    const int kk = A.k;
+    const bool track = kk <= D_UBK;
+    float ubk = INFINITY;  // k-th smallest UB seen: a proven bound on the query's k-th best
+    float ubl[D_UBK];
+    int nub = 0;
+    int cur_m = -1, m;
+    int64_t t, local = 0;
+    for (int64_t j = 0; dense_item(j, mt, A.n_tiles, m, t); ++j, ++local) {
+      if (m != cur_m) {  // only with more query tiles than CTAs
+        cur_m = m;
+        ubk = INFINITY;
+        nub = 0;
+      }
       const int acc = (int)(local & 1);
       const uint32_t aph = (uint32_t)((local >> 1) & 1);
       float2* ser = s_ser2 + acc * DN;     // (-2 inv, |x^|^2), +inf |x^|^2 past the last row
@@ -306,13 +335,9 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       const bool qv = slot < qd;
       const float4 qp = qv ? A.qparams[slot] : make_float4(0.f, 0.f, 0.f, 0.f);
       const float eps = fmaf(qp.z, tmx[0], qp.w + tmx[1]) + fabsf(qp.y) * tmx[2];
-      float thr = qv ? *(volatile float*)&A.thr[slot] : -INFINITY;
+      float thr = qv ? fminf(*(volatile float*)&A.thr[slot], ubk) : -INFINITY;
       float thr_e = thr + eps;
-      const int kk = A.k;
-      const bool track = kk <= D_UBK;
-      float ubk = INFINITY;  // k-th smallest approx' of this item's rows: ubk + eps bounds the k-th best
-      float ubl[D_UBK];
-      int nub = 0;
+      float ubk_ap = ubk - eps;  // a row improves the UB list iff approx' < ubk - eps
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(eq * 32) << 16) + (uint32_t)(acc * DN + half * (DN / 2));
@@ -332,7 +357,10 @@ __global__ void __launch_bounds__(D_THREADS, 1)
           cur[j] = __float_as_uint(ap);
           amin = fminf(amin, ap);
           if constexpr (!KONE) {
-            if (track && ap < ubk) ub_insert(ubl, nub, ubk, kk, ap);
+            if (track && ap < ubk_ap) {
+              ub_insert(ubl, nub, ubk, kk, ap + eps);
+              ubk_ap = ubk - eps;
+            }
           }
         }
         if (__any_sync(FULL, amin <= thr_e)) {
@@ -340,8 +368,8 @@ __global__ void __launch_bounds__(D_THREADS, 1)
           for (int j = 0; j < 32; ++j)
             emit_candidate(A, __uint_as_float(cur[j]) <= thr_e, slot, (uint32_t)(t * DN + col0 + j));
         }
-        if constexpr (KONE) ubk = fminf(ubk, amin);
-        thr = fminf(thr, fmaxf(ubk + eps, 0.f));
+        if constexpr (KONE) ubk = fminf(ubk, amin + eps);
+        thr = fminf(thr, fmaxf(ubk, 0.f));
         thr_e = thr + eps;
         if (c + 1 < DN / 64) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       }
