@@ -48,12 +48,23 @@ def parse():
     return p.parse_args()
 
 
+TF32_PER_BF16 = 1.1 / 2.25  # nominal dense TF32 : BF16 tensor throughput (B200_PROFILING.md)
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         d = json.load(open(path))
         return float(d["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
+
+
+def tensor_peak():
+    """bf16 dense TFLOP/s: measured burst (MEASURED_PEAKS.json) else the guide's fallback."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        return float(json.load(open(path))["bf16_tflops"])
+    return 1590.0
 
 
 class Clocks:
@@ -243,19 +254,39 @@ def main():
     ms_per_step = tot_ms / a.steps
     value = w.n_queries * a.steps / (tot_ms / 1e3)
 
-    # ---------------------------------------------------------------- roofline of the query kernel
+    # ---------------------------------------------------------------- roofline of the dominant kernel
+    # Per-kernel GPU times come from the library's CUDA events on the launching stream (sofa_knn
+    # with stats, same launch configuration as the timed steps): front (a5-a8 per query), dense
+    # pass (tcgen05 TF32 screen + exact refine, f1) and scan (a7-a8 task pool).
     hbm, peak_kind = peaks()
+    bf16 = tensor_peak()
+    km = st["kernel_ms"]
     l_b, n_b = w.l, 4 * w.length
-    # algorithmic bytes (SURVEY 8(d) unit costs): envelope nodes the tree descent evaluated (2l B each),
-    # words of surviving blocks (l B each), refined rows (4n B each), the query rows (4n B each)
-    alg_bytes = (st["env_nodes"] * 2 * l_b + st["words_scanned"] * l_b + st["refined"] * n_b
-                 + st["queries"] * n_b)
-    kern_ms = statistics.median(times)   # at N=1 the step is the query kernel (+ a 4-byte memset)
-    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    # sparse path (front + scan): algorithmic bytes = envelope nodes (2l B) + words scanned (l B)
+    # + rows refined (4n B) + query rows (4n B)  (SURVEY 8(d) unit costs)
+    sparse_bytes = (st["env_nodes"] * 2 * l_b + st["words_scanned"] * l_b + st["refined"] * n_b
+                    + st["queries"] * n_b)
+    sparse_ms = km["front"] + km["scan"]
+    sparse = {"bound": "hbm", "achieved": sparse_bytes / (sparse_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+              "kernel": "k_query front + scan (a5-a8)", "kernel_ms": sparse_ms, "algorithmic_bytes_per_launch": sparse_bytes}
+    sparse["frac"] = sparse["achieved"] / hbm
+    rooflines = [sparse]
+    if st["dense_queries"] > 0 and km["dense"] > 0:
+        # dense pass: 2 * queries * rows * n flops of the TF32 GEMM (the exact refine is tiny)
+        flops = 2.0 * st["dense_queries"] * (hi - lo) * w.length
+        tf32_peak = bf16 * TF32_PER_BF16
+        dn = {"bound": "tensor", "achieved": flops / (km["dense"] / 1e3) / 1e12, "peak": tf32_peak, "unit": "TFLOP/s",
+              "kernel": "k_dense_screen + k_dense_post (tcgen05 kind::tf32)", "kernel_ms": km["dense"],
+              "algorithmic_flops_per_launch": flops,
+              "peak_note": "measured bf16 burst x 1.1/2.25 (nominal dense TF32/BF16 ratio)"}
+        dn["frac"] = dn["achieved"] / tf32_peak
+        rooflines.append(dn)
+    dominant = max(rooflines, key=lambda r: r["kernel_ms"])
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{a.config}.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    roofline = dict(dominant, traffic=traffic, peak_kind=peak_kind, share_of_step=dominant["kernel_ms"] / sum(km.values()))
 
     # ---------------------------------------------------------------- e2e through the host C call
     e2e = None
@@ -314,10 +345,7 @@ def main():
                       "words_scanned_per_query": st["words_scanned"] / st["queries"]},
             "knn_stats": st,
             "build": {"ms": build_ms, "gb_per_s_series_read": (hi - lo) * w.length * 4 / (build_ms / 1e3) / 1e9},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "k_query (a5-a8 fused)", "algorithmic_bytes_per_launch": alg_bytes,
-                         "kernel_ms": kern_ms},
+            "roofline": roofline, "roofline_all": rooflines, "kernel_ms": km,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)

@@ -114,6 +114,8 @@ typedef struct {
   int64_t dense_refined;    /* exact distances computed by the dense path (incl. fallback rescans) */
   int64_t scan_tasks;       /* leaf chunks the front published to the scan pool (spread over all CTAs) */
   int64_t scan_queries;     /* queries that published at least one scan task */
+  double kernel_ms[3];      /* GPU time (CUDA events on the call's stream) of the front kernel, the
+                               dense pass (screen + exact refine) and the scan kernel */
 } sofa_knn_stats;
 
 /* Fill *out with defaults (sample_ratio 0.01, block_size 256, equi-depth, everything else 0). */

@@ -329,17 +329,33 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
     if ((rc = ensure_dense_scratch(ix, q, k))) return rc;
     SOFA_CK(cudaMemsetAsync(ix->dense.counters, 0, 64, st));
   }
+  // with stats: CUDA events on `st` around each launch group (front, dense pass, scan)
+  cudaEvent_t ev[4] = {};
+  if (stats)
+    for (auto& e : ev) SOFA_CK(cudaEventCreate(&e));
+  if (stats) SOFA_CK(cudaEventRecord(ev[0], st));
   if (ix->n == 0) {
     rc = launch_fill_pad(out_dist_dev, out_idx_dev, (int64_t)q * k, st);
+    if (stats) {
+      cudaEventRecord(ev[1], st);
+      cudaEventRecord(ev[2], st);
+    }
   } else {
     // front (per query) -> dense pass for flagged queries if the batch warrants it -> scan tasks
     // (every other leaf chunk of every query, spread over all CTAs); the dense and scan kernels read
     // the batch decision from device counters, so there is no host synchronisation in between
     rc = launch_query(ix, queries_dev, q, k, bsf_init_dev, out_dist_dev, out_idx_dev, st, false);
+    if (stats) cudaEventRecord(ev[1], st);
     if (!rc && dense) rc = launch_dense(ix, q, k, out_dist_dev, out_idx_dev, stats != nullptr, st);
+    if (stats) cudaEventRecord(ev[2], st);
     if (!rc) rc = launch_query(ix, queries_dev, q, k, bsf_init_dev, out_dist_dev, out_idx_dev, st, true);
   }
-  if (rc) return rc;
+  if (stats) cudaEventRecord(ev[3], st);
+  if (rc) {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    return rc;
+  }
   if (stats) {
     unsigned long long h[32] = {};
     SOFA_CK(cudaMemcpyAsync(h, ix->dstats, 32 * 8, cudaMemcpyDeviceToHost, st));
@@ -365,6 +381,12 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
     stats->dense_refined = (int64_t)h[21];
     stats->scan_tasks = (int64_t)h[22];
     stats->scan_queries = (int64_t)h[23];
+    for (int i = 0; i < 3; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      stats->kernel_ms[i] = ms;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
   }
   return SOFA_OK;
 }

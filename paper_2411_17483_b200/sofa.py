@@ -59,11 +59,13 @@ class sofa_knn_stats(C.Structure):
                                          "candidates", "refined", "abandoned", "env_nodes", "list_blocks",
                                          "rounds", "batches", "waves")] + [("phase_cycles", C.c_int64 * 4)] + \
         [(f, C.c_int64) for f in ("max_query_cycles", "max_list_blocks", "max_batches", "dense_queries",
-                                  "dense_candidates", "dense_refined", "scan_tasks", "scan_queries")]
+                                  "dense_candidates", "dense_refined", "scan_tasks", "scan_queries")] + \
+        [("kernel_ms", C.c_double * 3)]
 
     def to_dict(self) -> dict:
-        d = {f: int(getattr(self, f)) for f, _ in self._fields_ if f != "phase_cycles"}
+        d = {f: int(getattr(self, f)) for f, _ in self._fields_ if f not in ("phase_cycles", "kernel_ms")}
         d["phase_cycles"] = dict(zip(("prep", "seed", "tree", "scan_refine"), map(int, self.phase_cycles)))
+        d["kernel_ms"] = dict(zip(("front", "dense", "scan"), map(float, self.kernel_ms)))
         return d
 
 
