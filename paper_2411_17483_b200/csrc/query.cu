@@ -32,6 +32,8 @@ namespace sofa {
 constexpr int CAP_B = 2048;  // surviving blocks sorted in shared memory
 constexpr int CAP_C = 2048;  // words per scan batch (l <= 16)
 constexpr int CAPC = 4096;   // candidate buffer: one batch + candidates pending from earlier batches
+constexpr int TOPM_MIN_LEAVES = 256;  // top-M seeding for queries whose leaf list is longer than this
+constexpr int TOPM_LEAVES = 64;       // ... over (about) this many lowest-LB leaves
 constexpr int KMAX = SOFA_MAX_K;
 constexpr int kFan = 16;  // envelope tree fan-out
 
@@ -196,7 +198,9 @@ __device__ void topk_insert(const QArgs& A, QShared& S, float* s_tkd, int* s_tki
     const int k = A.k;
     const int n = *(volatile int*)&h->tkn;
     float b = INFINITY;
-    if (n < k || d < td[n - 1] || (d == td[n - 1] && i < ti[n - 1])) {
+    bool dup = false;  // a row refined twice (top-M seeding, then the scan) enters once
+    for (int p = 0; p < n; ++p) dup |= ti[p] == i;
+    if (!dup && (n < k || d < td[n - 1] || (d == td[n - 1] && i < ti[n - 1]))) {
       int p = n < k ? n : k - 1;
       while (p > 0 && (td[p - 1] > d || (td[p - 1] == d && ti[p - 1] > i))) {
         td[p] = td[p - 1];
@@ -225,7 +229,9 @@ __device__ void topk_insert(const QArgs& A, QShared& S, float* s_tkd, int* s_tki
   __threadfence_block();
   const int k = A.k;
   const int n = S.tkn;
-  if (n < k || d < s_tkd[n - 1] || (d == s_tkd[n - 1] && i < s_tki[n - 1])) {
+  bool dup = false;  // a row refined twice (top-M seeding, then the scan) enters once
+  for (int p = 0; p < n; ++p) dup |= s_tki[p] == i;
+  if (!dup && (n < k || d < s_tkd[n - 1] || (d == s_tkd[n - 1] && i < s_tki[n - 1]))) {
     int p = n < k ? n : k - 1;
     while (p > 0 && (s_tkd[p - 1] > d || (s_tkd[p - 1] == d && s_tki[p - 1] > i))) {
       s_tkd[p] = s_tkd[p - 1];
@@ -625,9 +631,107 @@ __device__ void filter_list(const unsigned long long* src, int cnt, float thr, f
       const int slot = base + __popc(m & ((1u << lane) - 1u));
       const bool got = tk && slot < cap;
       if (got) take[slot] = ent[u];
-      warp_append(keep && !got, ent[u], rem, nrem);
+      if (rem) warp_append(keep && !got, ent[u], rem, nrem);
     }
   }
+}
+
+// Top-M seeding (SURVEY SIM-6): word LBs of the leaves in `list` (LB only, no refinement), then
+// only the M = 32 lowest-LB words are refined (each warp keeps its 4 lowest in registers and
+// refines them).  The lowest word LBs of the most promising leaves almost always include the true
+// nearest neighbour, so the BSF is (nearly) final before the real scan starts — instead of being
+// tightened one greedy batch at a time from the own-key seed.
+template <int LT, int NF>
+__device__ void seed_topm(const QArgs& A, QShared& S, const unsigned long long* list, int cnt, const float* s_T,
+                          float* s_tkd, int* s_tki, const float4* s_qh4) {
+  constexpr int NC = LT / 16;
+  constexpr int WMAX = 8 / NC;
+  constexpr int M = 4;  // per warp
+  constexpr int NW = kThreads / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int B = A.B;
+  int ppl = B / (32 * WMAX);
+  if (ppl < 1) ppl = 1;
+  const int span = B / ppl, wpl = span / 32;
+  const float thr = S.thr;
+  unsigned long long best[M];
+#pragma unroll
+  for (int r = 0; r < M; ++r) best[r] = ~0ull;
+  unsigned n_words = 0;
+  for (int u = warp; u < cnt * ppl; u += NW) {
+    const unsigned long long ent = list[u / ppl];
+    const int64_t base = (int64_t)(uint32_t)ent * B + (int64_t)(u % ppl) * span;
+#pragma unroll
+    for (int i = 0; i < WMAX; ++i) {
+      const int64_t pos = base + i * 32 + lane;
+      if (i < wpl && pos < A.n) {
+        uint4 wr[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) wr[c] = ld_stream_u4(A.words + pos * A.WS + 16 * c);
+        const float lb = word_lb<LT>(reinterpret_cast<const uint4(&)[NC]>(wr), s_T, thr);
+        ++n_words;
+        unsigned long long key = lb <= thr ? pack(lb, (uint32_t)pos) : ~0ull;
+#pragma unroll
+        for (int r = 0; r < M; ++r)  // insert into this lane's sorted best-M
+          if (key < best[r]) {
+            const unsigned long long t = best[r];
+            best[r] = key;
+            key = t;
+          }
+      }
+    }
+  }
+  // the warp's M lowest: M rounds of warp-min over the lanes' list heads
+  const float* rows[M];
+  float2 st[M];
+  bool on[M];
+  int oidx[M];
+#pragma unroll
+  for (int r = 0; r < M; ++r) {
+    unsigned long long m = best[0];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(FULL, m, o);
+      m = other < m ? other : m;
+    }
+    on[r] = m != ~0ull;
+    if (on[r] && best[0] == m) {  // the owner pops its head (keys are unique: they hold the position)
+#pragma unroll
+      for (int s = 0; s < M - 1; ++s) best[s] = best[s + 1];
+      best[M - 1] = ~0ull;
+    }
+    oidx[r] = -1;
+    rows[r] = A.series;
+    st[r] = make_float2(0.f, 0.f);
+    if (on[r]) {
+      const uint32_t pos = (uint32_t)m;
+      oidx[r] = A.perm[pos];
+      st[r] = A.stats[pos];
+      rows[r] = A.series + (int64_t)oidx[r] * A.len;
+    }
+  }
+  float bsf = 0.f;
+  if (lane == 0) bsf = *(volatile float*)&S.bsf;
+  bsf = __shfl_sync(FULL, bsf, 0);
+  float d2[M];
+  bool ab[M];
+  ed_warp_multi<NF, M>(rows, st, on, s_qh4, A.len >> 2, bsf, d2, ab);
+  if (lane == 0) {
+    unsigned n_ref = 0;
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      if (!on[r]) continue;
+      ++n_ref;
+      if (ab[r]) continue;
+      const int n = *(volatile int*)&S.tkn;
+      const float kd = *(volatile float*)&s_tkd[n > 0 ? n - 1 : 0];
+      if (n < A.k || d2[r] <= kd) topk_insert(A, S, s_tkd, s_tki, d2[r], oidx[r]);
+    }
+    if (n_ref) atomicAdd(&S.st[3], n_ref);
+  }
+  n_words = __reduce_add_sync(FULL, n_words);
+  if (lane == 0 && n_words) atomicAdd(&S.st[1], n_words);
+  __syncthreads();
 }
 
 template <int LT, int NF>
@@ -656,7 +760,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const __grid_constant__ Q
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int len = A.len, nf4 = len >> 2, l = A.l, a = A.a;
-  unsigned long long* gl = A.gscratch + (int64_t)blockIdx.x * 2 * A.nb;
+  unsigned long long* gl = A.gscratch + (int64_t)blockIdx.x * 2 * A.nb;  // the two halves swap roles
   unsigned long long* gl2 = gl + A.nb;
 
   if (A.mode == 1) {
@@ -800,40 +904,55 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const __grid_constant__ Q
     {
       int cnt = S.cnt;
       if (tid == 0) S.st[6] += cnt;
+      if (cnt > TOPM_MIN_LEAVES) {
+        // top-M seeding over the TOPM_LEAVES lowest-LB leaves (threshold from a sorted strided sample)
+        s_cand[tid] = gl[((int64_t)tid * cnt) / kThreads];
+        if (tid == 0) S.take = 0;
+        __syncthreads();
+        bitonic_sort_u64(s_cand, kThreads);
+        int r = (int)(((int64_t)kThreads * TOPM_LEAVES) / cnt);
+        r = r < 0 ? 0 : (r > kThreads - 1 ? kThreads - 1 : r);
+        const float tau = lb_of(s_cand[r]);
+        filter_list(gl, cnt, S.thr, tau, s_blist, &S.take, nullptr, nullptr, TOPM_LEAVES);
+        __syncthreads();
+        const int nt = S.take < TOPM_LEAVES ? S.take : TOPM_LEAVES;
+        seed_topm<LT, NF>(A, S, s_blist, nt, s_T, s_tkd, s_tki, s_qh4);
+        // re-filter the leaf list against the (nearly final) BSF
+        if (tid == 0) {
+          S.take = 0;
+          S.rem = 0;
+        }
+        __syncthreads();
+        filter_list(gl, cnt, S.thr, -1.f, s_blist, &S.take, gl2, &S.rem);
+        __syncthreads();
+        cnt = S.rem;
+        unsigned long long* t = gl;
+        gl = gl2;
+        gl2 = t;
+      }
       if (tid == 0) {
         s_dense = -1;
         s_dec[0] = s_dec[1] = s_dec[2] = s_dec[3] = 0;
       }
       __syncthreads();  // every thread must see -1 before the (uniform) branch below
       if (A.dense_min > 0 && cnt >= A.dense_min) {
-        // f1 decision: refine the TAKE0 lowest-LB leaves first (tightens the BSF, as MESSI's first
-        // DeleteMin rounds do), re-filter the rest against it; if >= dense_min leaves still survive,
-        // the SFA bound cannot prune this query and it goes to the batched dense path.
+        // f1 decision, after top-M seeding: sample the words of the TAKE0 lowest-LB leaves (they stay in
+        // the list); if most of them still pass the (nearly final) BSF and many leaves survive, the
+        // SFA bound cannot prune this query and it goes to the batched dense path.
         constexpr int TAKE0 = 8;
         s_cand[tid] = gl[((int64_t)tid * cnt) / kThreads];
-        if (tid == 0) {
-          S.take = 0;
-          S.rem = 0;
-        }
+        if (tid == 0) S.take = 0;
         __syncthreads();
         bitonic_sort_u64(s_cand, kThreads);
         int r = (int)(((int64_t)kThreads * TAKE0) / cnt);
         r = r < 0 ? 0 : (r > kThreads - 1 ? kThreads - 1 : r);
         const float tau = lb_of(s_cand[r]);
-        filter_list(gl, cnt, S.thr, tau, s_blist, &S.take, gl2, &S.rem, TAKE0);
+        filter_list(gl, cnt, S.thr, tau, s_blist, &S.take, nullptr, nullptr, TAKE0);
         __syncthreads();
         const int ntake = S.take < TAKE0 ? S.take : TAKE0;
-        const int nrem = S.rem;
-        bitonic_sort_u64(s_blist, ntake);
-        scan_blocks<LT, NF>(A, S, s_blist, ntake, true, s_T, s_tkd, s_tki, s_qh4);
-        if (tid == 0) {
-          S.take = 0;
-          S.rem = 0;
-        }
         __syncthreads();
-        filter_list(gl2, nrem, S.thr, -1.f, s_blist, &S.take, gl, &S.rem);
+        if (tid == 0) S.take = 0;
         __syncthreads();
-        cnt = S.rem;
         // power of the SFA bound on this query: the fraction of the take blocks' words whose LB is
         // still <= the tightened threshold (high-frequency data ~1, noisy members ~1e-3).  Dense only
         // if many leaves survive AND most of their words would have to be refined anyway.
@@ -860,7 +979,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const __grid_constant__ Q
             s_dec[2] = S.take;
             s_dec[3] = nw;
           }
-          if (tid == 0 && (A.dense_force || est * 32.0 >= (double)A.n)) {
+          if (tid == 0 && (A.dense_force || est * 8.0 >= (double)A.n)) {
             s_dense = atomicAdd(A.qd_counter, 1);
             s_dec[0] = 1;
             atomicAdd(reinterpret_cast<unsigned long long*>(A.qd_counter + 6),
