@@ -322,6 +322,10 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
       }
       thr = __shfl_sync(FULL, thr, 0);
       bsf = __shfl_sync(FULL, bsf, 0);
+      bool mine = false;
+#pragma unroll
+      for (int i = 0; i < WMAX; ++i) mine |= lbv[i] <= thr;
+      if (!__any_sync(FULL, mine)) break;  // the common case: no candidate left in this unit
       const float* rows[R];
       float2 st[R];
       bool on[R];
