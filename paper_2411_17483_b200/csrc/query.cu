@@ -31,7 +31,6 @@ namespace sofa {
 
 constexpr int CAP_B = 2048;  // surviving blocks sorted in shared memory
 constexpr int CAP_C = 2048;  // words per scan batch (l <= 16)
-constexpr int CAPC = 4096;   // candidate buffer: one batch + candidates pending from earlier batches
 constexpr int TOPM_MIN_LEAVES = 256;  // top-M seeding for queries whose leaf list is longer than this
 constexpr int TOPM_LEAVES = 64;       // ... over (about) this many lowest-LB leaves
 constexpr int KMAX = SOFA_MAX_K;
@@ -447,8 +446,7 @@ __device__ void publish_tasks(const QArgs& A, QShared& S, int q, const unsigned 
 // scan mode: all CTAs pull tasks until the pool is drained; rank-major order (every query's lowest-
 // LB chunk first), so a query's later chunks usually meet its final BSF and are rejected unread
 template <int LT, int NF>
-__device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, unsigned long long* s_cand, float* s_tkd, int* s_tki,
-                           float* s_wd, int* s_wi, float4* s_qh4) {
+__device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd, int* s_tki, float4* s_qh4) {
   const int tid = threadIdx.x;
   bool dense_go = false;
   if (A.qd_counter) {
@@ -739,7 +737,7 @@ __device__ void seed_topm(const QArgs& A, QShared& S, const unsigned long long* 
 }
 
 template <int LT, int NF>
-__global__ void __launch_bounds__(kThreads, 2) k_query(const __grid_constant__ QArgs A) {
+__global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ QArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ QShared S;
   constexpr int UB0 = 2 * LT * 256 * 4, UB1 = CAP_B * 8, UB2 = NF * 128 * 8;
@@ -752,11 +750,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const __grid_constant__ Q
   float* s_Thi = s_Tlo + LT * 256;
   double* s_qd = reinterpret_cast<double*>(s_u);
   unsigned long long* s_blist = reinterpret_cast<unsigned long long*>(s_u);
-  unsigned long long* s_cand = reinterpret_cast<unsigned long long*>(s_u + UB);
-  float* s_tkd = reinterpret_cast<float*>(s_cand + CAPC);
+  unsigned long long* s_samp = reinterpret_cast<unsigned long long*>(s_u + UB);  // strided list sample
+  float* s_tkd = reinterpret_cast<float*>(s_samp + kThreads);
   int* s_tki = reinterpret_cast<int*>(s_tkd + KMAX);
-  float* s_wd = reinterpret_cast<float*>(s_tki + KMAX);
-  int* s_wi = reinterpret_cast<int*>(s_wd + 8);
   __shared__ uint8_t s_qw[SOFA_MAX_L];
   __shared__ unsigned long long s_seed;
   __shared__ int s_dense;
@@ -768,7 +764,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const __grid_constant__ Q
   unsigned long long* gl2 = gl + A.nb;
 
   if (A.mode == 1) {
-    scan_tasks<LT, NF>(A, S, s_T, s_cand, s_tkd, s_tki, s_wd, s_wi, s_qh4);
+    scan_tasks<LT, NF>(A, S, s_T, s_tkd, s_tki, s_qh4);
     return;
   }
   for (;;) {
@@ -910,13 +906,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const __grid_constant__ Q
       if (tid == 0) S.st[6] += cnt;
       if (cnt > TOPM_MIN_LEAVES) {
         // top-M seeding over the TOPM_LEAVES lowest-LB leaves (threshold from a sorted strided sample)
-        s_cand[tid] = gl[((int64_t)tid * cnt) / kThreads];
+        s_samp[tid] = gl[((int64_t)tid * cnt) / kThreads];
         if (tid == 0) S.take = 0;
         __syncthreads();
-        bitonic_sort_u64(s_cand, kThreads);
+        bitonic_sort_u64(s_samp, kThreads);
         int r = (int)(((int64_t)kThreads * TOPM_LEAVES) / cnt);
         r = r < 0 ? 0 : (r > kThreads - 1 ? kThreads - 1 : r);
-        const float tau = lb_of(s_cand[r]);
+        const float tau = lb_of(s_samp[r]);
         filter_list(gl, cnt, S.thr, tau, s_blist, &S.take, nullptr, nullptr, TOPM_LEAVES);
         __syncthreads();
         const int nt = S.take < TOPM_LEAVES ? S.take : TOPM_LEAVES;
@@ -944,13 +940,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const __grid_constant__ Q
         // the list); if most of them still pass the (nearly final) BSF and many leaves survive, the
         // SFA bound cannot prune this query and it goes to the batched dense path.
         constexpr int TAKE0 = 8;
-        s_cand[tid] = gl[((int64_t)tid * cnt) / kThreads];
+        s_samp[tid] = gl[((int64_t)tid * cnt) / kThreads];
         if (tid == 0) S.take = 0;
         __syncthreads();
-        bitonic_sort_u64(s_cand, kThreads);
+        bitonic_sort_u64(s_samp, kThreads);
         int r = (int)(((int64_t)kThreads * TAKE0) / cnt);
         r = r < 0 ? 0 : (r > kThreads - 1 ? kThreads - 1 : r);
-        const float tau = lb_of(s_cand[r]);
+        const float tau = lb_of(s_samp[r]);
         filter_list(gl, cnt, S.thr, tau, s_blist, &S.take, nullptr, nullptr, TAKE0);
         __syncthreads();
         const int ntake = S.take < TAKE0 ? S.take : TAKE0;
@@ -1045,16 +1041,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_query(const __grid_constant__ Q
         publish_tasks<LT>(A, S, qi, s_blist + nloc, rest, true, dc);
       } else {
         if (tid == 0) S.st[7] += 1;
-        s_cand[tid] = gl[((int64_t)tid * cnt) / kThreads];
+        s_samp[tid] = gl[((int64_t)tid * cnt) / kThreads];
         if (tid == 0) {
           S.take = 0;
           S.rem = 0;
         }
         __syncthreads();
-        bitonic_sort_u64(s_cand, kThreads);
+        bitonic_sort_u64(s_samp, kThreads);
         int r = (int)(((int64_t)kThreads * (CAP_B * 3 / 4)) / cnt);
         r = r < 0 ? 0 : (r > kThreads - 1 ? kThreads - 1 : r);
-        const float tau = lb_of(s_cand[r]);
+        const float tau = lb_of(s_samp[r]);
         filter_list(gl, cnt, S.thr, tau, s_blist, &S.take, gl2, &S.rem);
         __syncthreads();
         const int ntake = S.take < CAP_B ? S.take : CAP_B;
@@ -1134,7 +1130,7 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
   QArgs A = A0;
   constexpr int UB0 = 2 * LT * 256 * 4, UB1 = CAP_B * 8, UB2 = NF * 128 * 8;
   constexpr int UB = UB0 > UB1 ? (UB0 > UB2 ? UB0 : UB2) : (UB1 > UB2 ? UB1 : UB2);
-  const size_t smem = NF * 128 * 4 + LT * 8 + LT * 256 * 4 + UB + CAPC * 8 + KMAX * 8 + 8 * 8;
+  const size_t smem = NF * 128 * 4 + LT * 8 + LT * 256 * 4 + UB + kThreads * 8 + KMAX * 8;
   auto kern = k_query<LT, NF>;
   SOFA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0, sms = 148;
