@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--n-series", type=int, default=0, help="override N (debug only; changes the workload)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-flush", action="store_true",
+                   help="diagnostic: skip the L2 flush between timed steps (inputs are larger than L2 anyway)")
     return p.parse_args()
 
 
@@ -234,7 +236,8 @@ def main():
     launches0 = S.sofa_launch_count()
     with Clocks(local) as clk:
         for s in range(a.steps):
-            flush_l2(l2)
+            if not a.no_flush:
+                flush_l2(l2)
             barrier()
             torch.cuda.synchronize()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -338,7 +341,7 @@ def main():
             "config": {"workload": w.name, "n_series": N, "length": w.length, "l": w.l, "alphabet": w.alphabet,
                        "k": w.k, "queries": w.n_queries, "block_size": 256,
                        "sample_size": datagen.default_sample_size(w),
-                       "l2": "flushed between timed steps (512 MB write)", "parallelism": f"shard{world}"},
+                       "l2": "not flushed (inputs larger than L2)" if a.no_flush else "flushed between timed steps (512 MB write)", "parallelism": f"shard{world}"},
             "prune": {"series": 1.0 - st["refined"] / (st["queries"] * (hi - lo)),
                       "block": 1.0 - st["blocks_survived"] / max(1, st["blocks_total"]),
                       "refined_per_query": st["refined"] / st["queries"],

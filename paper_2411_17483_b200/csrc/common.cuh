@@ -200,6 +200,9 @@ struct DenseScratch {
   int* ovf_list = nullptr;
   unsigned long long* cand = nullptr;
   int* counters = nullptr;
+  alignas(64) unsigned char tmap_q[128];  // CUtensorMap of qhat (q x len), encoded for tmap_q_rows rows
+  alignas(64) unsigned char tmap_x[128];  // CUtensorMap of the series (n x len)
+  int tmap_q_rows = -1;
 };
 
 // Host-side index object (opaque in the C ABI).

@@ -555,10 +555,14 @@ static int make_tmap(CUtensorMap* m, const float* base, int64_t rows, int len, i
 
 int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stats, cudaStream_t st) {
   DenseScratch& D = ix->dense;
-  CUtensorMap tmQ, tmX;
   int rc;
-  if ((rc = make_tmap(&tmQ, D.qhat, q, ix->len, DM))) return rc;
-  if ((rc = make_tmap(&tmX, ix->series, ix->n, ix->len, DN))) return rc;
+  if (D.tmap_q_rows != q) {  // tensor maps are encoded once per buffer (not on every call)
+    if ((rc = make_tmap(reinterpret_cast<CUtensorMap*>(D.tmap_q), D.qhat, q, ix->len, DM))) return rc;
+    if ((rc = make_tmap(reinterpret_cast<CUtensorMap*>(D.tmap_x), ix->series, ix->n, ix->len, DN))) return rc;
+    D.tmap_q_rows = q;
+  }
+  const CUtensorMap& tmQ = *reinterpret_cast<const CUtensorMap*>(D.tmap_q);
+  const CUtensorMap& tmX = *reinterpret_cast<const CUtensorMap*>(D.tmap_x);
   DenseArgs A{};
   A.n = ix->n;
   A.dense_rows = dense_batch_rows(ix);
@@ -577,9 +581,12 @@ int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stat
   A.ovf_list = D.ovf_list;
   A.ovf_count = D.counters + 1;
   auto screen = k == 1 ? k_dense_screen<true> : k_dense_screen<false>;
-  SOFA_CK(cudaFuncSetAttribute(screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D_SMEM));
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+  static int cached_dev[2] = {-1, -1}, sms = 148;
+  if (cached_dev[k == 1] != ix->device) {
+    SOFA_CK(cudaFuncSetAttribute(screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D_SMEM));
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+    cached_dev[k == 1] = ix->device;
+  }
   screen<<<sms, D_THREADS, D_SMEM, st>>>(tmQ, tmX, A);
   SOFA_LAUNCHED();
 
@@ -631,6 +638,7 @@ int ensure_dense_scratch(sofa_index* ix, int q, int k) {
   DenseScratch& D = ix->dense;
   if (D.q_cap >= q && D.k_cap >= k && D.len == ix->len) return SOFA_OK;
   free_dense_scratch(ix);
+  D.tmap_q_rows = -1;
   D.q_cap = q;
   D.k_cap = k;
   D.len = ix->len;

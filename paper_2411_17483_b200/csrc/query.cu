@@ -1132,11 +1132,15 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
   constexpr int UB = UB0 > UB1 ? (UB0 > UB2 ? UB0 : UB2) : (UB1 > UB2 ? UB1 : UB2);
   const size_t smem = NF * 128 * 4 + LT * 8 + LT * 256 * 4 + UB + kThreads * 8 + KMAX * 8;
   auto kern = k_query<LT, NF>;
-  SOFA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0, sms = 148;
-  SOFA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
-  if (per_sm < 1) per_sm = 1;
+  // launch shape, once per instantiation and device (no driver queries on the per-call path)
+  static int cached_dev = -1, per_sm = 0, sms = 148;
+  if (cached_dev != ix->device) {
+    SOFA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SOFA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+    if (per_sm < 1) per_sm = 1;
+    cached_dev = ix->device;
+  }
   // the whole GPU even for a small batch: CTAs without a query of their own help heavy ones
   const int grid = sms * per_sm;
   const int64_t need = (int64_t)grid * 2 * (ix->nb > 0 ? ix->nb : 1);
