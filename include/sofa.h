@@ -52,6 +52,10 @@ extern "C" {
 
 #define SOFA_BINNING_EQUI_DEPTH 0 /* BASELINE.json */
 #define SOFA_BINNING_EQUI_WIDTH 1 /* Alg. 1 l.8-11 */
+#define SOFA_BINNING_ISAX 2       /* the iSAX baseline summarization: l
+                                     PAA segments of n/l values (requires n % l == 0), N(0,1)
+                                     equal-depth breakpoints, mindist weight n/l per position.
+                                     Static: nothing is learned from the data. */
 
 /* Opaque index: owns the SFA words (sorted), per-series (mu, 1/sigma), the permutation,
  * per-block envelopes, block keys, the model's device tables and query scratch.  It BORROWS
@@ -65,7 +69,7 @@ typedef struct {
   int32_t len;       /* series length n */
   int32_t l;         /* number of selected real values = symbols per word (reading 4) */
   int32_t alphabet;  /* a */
-  int32_t binning;   /* SOFA_BINNING_* */
+  int32_t binning;   /* SOFA_BINNING_*; _ISAX: best_pos[j] = j is PAA segment j */
   int32_t best_pos[SOFA_MAX_L];   /* interleaved positions (2k = Re X_k, 2k+1 = Im X_k),
                                      descending sample variance, ties -> lower position */
   double weights[SOFA_MAX_L];     /* Eq. 1 weight per selected position: 1 (DC/Nyquist) or 2 */
@@ -77,7 +81,7 @@ typedef struct {
   double sample_ratio;     /* default 0.01 (Alg. 1 r) */
   int32_t block_size;      /* B series per leaf block, default 256 (reading 19) */
   int32_t candidate_limit; /* max complex index eligible for selection; 0 => n/2 (reading 3) */
-  int32_t binning;         /* SOFA_BINNING_EQUI_DEPTH (default) or _EQUI_WIDTH */
+  int32_t binning;         /* SOFA_BINNING_EQUI_DEPTH (default), _EQUI_WIDTH or _ISAX */
   int32_t dense_permille;  /* dense path for a query whose leaf list still keeps
                               >= this many permille of the blocks after its 8 lowest-LB leaves
                               were refined and >= 1/16 of their words still pass the tightened

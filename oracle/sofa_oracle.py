@@ -23,6 +23,8 @@ What each part computes (and what pins it, tests/test_oracle.py):
   knn_bruteforce   NN definition (reading 14), k-NN       pinned: pure-python loops,
                                                                          noisy-member known answers
   knn_gemini       GEMINI filter+refine              pinned: == brute force
+  paa / isax_*     the iSAX baseline: PAA segments, N(0,1)  pinned: textbook breakpoints,
+                   breakpoints, mindist weight n/l                      PAA closed forms, LB <= ED^2
 Nothing here is "parity unpinned".
 """
 from __future__ import annotations
@@ -157,10 +159,37 @@ def learn_model(sample: np.ndarray, l: int, a: int, binning: str = "equi-depth",
             "weights": position_weights(best, n), "binning": binning}
 
 
+# ----------------------------------------------------------------------------- iSAX baseline (f4)
+def paa(xhat: np.ndarray, l: int) -> np.ndarray:
+    """Segmentation + aggregation: means of l segments of equal length n/l."""
+    xhat = np.atleast_2d(np.asarray(xhat, dtype=F64))
+    m, n = xhat.shape
+    if n % l:
+        raise ValueError("iSAX needs n % l == 0")
+    return xhat.reshape(m, l, n // l).mean(axis=2)
+
+
+def isax_breakpoints(a: int) -> np.ndarray:
+    """Fixed quantization: equal-depth bins of N(0,1), beta_i = Phi^-1(i/a)."""
+    from scipy.stats import norm
+    return norm.ppf(np.arange(1, a) / a)
+
+
+def isax_model(n: int, l: int, a: int) -> dict:
+    """The iSAX summarization as a model: positions = PAA segments, the same breakpoints for every
+    segment, mindist weight n/l per segment (SAX mindist = sqrt(n/l) sqrt(sum dist^2))."""
+    e = isax_breakpoints(a)
+    return {"n": n, "l": l, "a": a, "best_pos": np.arange(l), "edges": np.stack([e] * l),
+            "weights": np.full(l, n / l), "binning": "isax"}
+
+
 # ----------------------------------------------------------------------------- a3 SFA transform
 def project(x: np.ndarray, model: dict) -> np.ndarray:
-    """Alg. 2 l.2-3: DFT of the z-normalised series, keep best_l positions."""
+    """Alg. 2 l.2-3: DFT of the z-normalised series, keep best_l positions
+    (for the iSAX baseline: the PAA of the z-normalised series)."""
     xh, _, _, _ = znorm(np.atleast_2d(x))
+    if model.get("binning") == "isax":
+        return paa(xh, model["l"])
     return spectrum(xh)[:, model["best_pos"]]
 
 

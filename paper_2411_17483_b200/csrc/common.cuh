@@ -259,6 +259,7 @@ int launch_gather(const uint8_t* words, const float2* stats, const int32_t* perm
                   uint8_t* words_out, float2* stats_out, cudaStream_t st);
 int learn_model_dev(const float* sample, int64_t S, int len, int l, int a, int binning, int cand_limit,
                     cudaStream_t st, sofa_model* out);
+int isax_model(int len, int l, int a, sofa_model* out);
 int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
                  cudaStream_t st, bool scan = false);
 // batch-level dense decision (f1): run the tensor-core pass iff the flagged queries' estimated sparse

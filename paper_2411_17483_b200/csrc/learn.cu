@@ -308,4 +308,57 @@ int learn_model_dev(const float* sample, int64_t S, int len, int l, int a, int b
   return SOFA_OK;
 }
 
+// Standard normal quantile Phi^-1(p): Acklam's rational approximation refined by two Halley steps on
+// erfc (double precision).
+static double norm_ppf(double p) {
+  static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                             1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                             6.680131188771972e+01, -1.328068155288572e+01};
+  static const double c[] = {-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+                             -2.549732539343734e+00, 4.374664141464968e+00, 2.938163982698783e+00};
+  static const double d[] = {7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+                             3.754408661907416e+00};
+  double x;
+  if (p < 0.02425) {
+    const double q = std::sqrt(-2 * std::log(p));
+    x = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1);
+  } else if (p > 1 - 0.02425) {
+    const double q = std::sqrt(-2 * std::log(1 - p));
+    x = -(((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1);
+  } else {
+    const double q = p - 0.5, r = q * q;
+    x = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1);
+  }
+  for (int it = 0; it < 2; ++it) {
+    const double e = 0.5 * std::erfc(-x / std::sqrt(2.0)) - p;
+    const double u = e * std::sqrt(2 * M_PI) * std::exp(x * x / 2);
+    x = x - u / (1 + x * u / 2);
+  }
+  return x;
+}
+
+// The iSAX baseline: l PAA segments of n/l values, breakpoints beta_i = Phi^-1(i/a)
+// (equal-depth under N(0,1)), mindist weight n/l (PAA lower-bounds ED by Cauchy-Schwarz per segment).
+int isax_model(int len, int l, int a, sofa_model* out) {
+  if (len % l != 0) {
+    set_error("iSAX needs len % l == 0 (segments of equal length n/l)");
+    return SOFA_EINVAL;
+  }
+  memset(out, 0, sizeof(*out));
+  out->len = len;
+  out->l = l;
+  out->alphabet = a;
+  out->binning = SOFA_BINNING_ISAX;
+  for (int j = 0; j < l; ++j) {
+    out->best_pos[j] = j;
+    out->weights[j] = (double)len / l;
+    for (int i = 1; i < a; ++i) out->edges[j * 255 + i - 1] = norm_ppf((double)i / a);
+  }
+  return SOFA_OK;
+}
+
 }  // namespace sofa

@@ -32,13 +32,17 @@ static int check_shape(int64_t len, int64_t l, int64_t a) {
 }
 
 // basis rows for the selected positions: [LT][len], rows >= l are zero
-__global__ void k_basis_sel(const int* __restrict__ pos, int l, int LT, int len, double* __restrict__ b64,
+// (iSAX: row j averages PAA segment j)
+__global__ void k_basis_sel(const int* __restrict__ pos, int l, int LT, int len, int isax, double* __restrict__ b64,
                             float* __restrict__ b32) {
   const double rs = 1.0 / sqrt((double)len);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < LT * len; i += gridDim.x * blockDim.x) {
     const int j = i / len, t = i % len;
     double v = 0.0;
-    if (j < l) {
+    if (j < l && isax) {
+      const int seg = len / l;
+      v = t / seg == pos[j] ? 1.0 / seg : 0.0;
+    } else if (j < l) {
       const int k = pos[j] >> 1, im = pos[j] & 1;
       const int m = (int)(((int64_t)k * t) % len);
       double sn, cs;
@@ -87,7 +91,8 @@ int upload_model(const sofa_model& m, int len, sofa_index* ix, cudaStream_t st) 
   int* dpos = nullptr;
   SOFA_CK(cudaMalloc(&dpos, SOFA_MAX_L * 4));
   SOFA_CK(cudaMemcpyAsync(dpos, m.best_pos, SOFA_MAX_L * 4, cudaMemcpyHostToDevice, st));
-  k_basis_sel<<<(LT * len + 255) / 256, 256, 0, st>>>(dpos, l, LT, len, ix->basis64, ix->basis32);
+  k_basis_sel<<<(LT * len + 255) / 256, 256, 0, st>>>(dpos, l, LT, len, m.binning == SOFA_BINNING_ISAX ? 1 : 0,
+                                                      ix->basis64, ix->basis32);
   cudaError_t e = cudaGetLastError();
   g_launches.fetch_add(1);
   cudaStreamSynchronize(st);
@@ -111,8 +116,10 @@ int upload_model(const sofa_model& m, int len, sofa_index* ix, cudaStream_t st) 
 static int validate_model(const sofa_model& m) {
   int rc = check_shape(m.len, m.l, m.alphabet);
   if (rc) return rc;
+  if (m.binning == SOFA_BINNING_ISAX && m.len % m.l != 0) return fail(SOFA_EINVAL, "iSAX needs len % l == 0");
   for (int j = 0; j < m.l; ++j) {
-    if (m.best_pos[j] < 0 || m.best_pos[j] >= m.len + 2) return fail(SOFA_EINVAL, "model best_pos out of range");
+    const int lim = m.binning == SOFA_BINNING_ISAX ? m.l : m.len + 2;
+    if (m.best_pos[j] < 0 || m.best_pos[j] >= lim) return fail(SOFA_EINVAL, "model best_pos out of range");
     for (int i = 1; i < m.alphabet - 1; ++i)
       if (!(m.edges[j * 255 + i] >= m.edges[j * 255 + i - 1])) return fail(SOFA_EINVAL, "model edges not ascending");
   }
@@ -146,7 +153,9 @@ int sofa_learn_model(const float* sample_dev, int64_t S, int32_t len, int32_t l,
   if (!sample_dev || !out) return fail(SOFA_EINVAL, "NULL pointer");
   const int binning = opts ? opts->binning : SOFA_BINNING_EQUI_DEPTH;
   const int cl = opts ? opts->candidate_limit : 0;
-  if (binning != SOFA_BINNING_EQUI_DEPTH && binning != SOFA_BINNING_EQUI_WIDTH) return fail(SOFA_EINVAL, "binning");
+  if (binning != SOFA_BINNING_EQUI_DEPTH && binning != SOFA_BINNING_EQUI_WIDTH && binning != SOFA_BINNING_ISAX)
+    return fail(SOFA_EINVAL, "binning");
+  if (binning == SOFA_BINNING_ISAX) return isax_model(len, l, alphabet, out);
   return learn_model_dev(sample_dev, S, len, l, alphabet, binning, cl, (cudaStream_t)cuda_stream, out);
 }
 
@@ -175,7 +184,8 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
   if (n > 2147483647LL) return fail(SOFA_EINVAL, "n must fit int32 per shard");
   if (!pow2(opts.block_size) || opts.block_size < 32 || opts.block_size > 8192)
     return fail(SOFA_EINVAL, "block_size must be a power of two in [32, 8192]");
-  if (opts.binning != SOFA_BINNING_EQUI_DEPTH && opts.binning != SOFA_BINNING_EQUI_WIDTH)
+  if (opts.binning != SOFA_BINNING_EQUI_DEPTH && opts.binning != SOFA_BINNING_EQUI_WIDTH &&
+      opts.binning != SOFA_BINNING_ISAX)
     return fail(SOFA_EINVAL, "binning");
   const int64_t gn = opts.global_n > 0 ? opts.global_n : n;
   if (opts.global_offset < 0 || opts.global_offset + n > gn) return fail(SOFA_EINVAL, "global_offset/global_n");
@@ -203,6 +213,8 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
     if (m.len != len || m.l != l || m.alphabet != alphabet) return bail(fail(SOFA_EINVAL, "opts->model disagrees with (len, l, alphabet)"));
     if ((rc = validate_model(m))) return bail(rc);
     ix->model = m;
+  } else if (opts.binning == SOFA_BINNING_ISAX) {  // static: nothing to learn
+    if ((rc = isax_model(len, l, alphabet, &ix->model))) return bail(rc);
   } else {
     if (n == 0) return bail(fail(SOFA_EINVAL, "n = 0 needs opts->model"));
     int64_t S = opts.sample_size > 0 ? opts.sample_size : (int64_t)llround(opts.sample_ratio * (double)gn);

@@ -16,7 +16,7 @@ from .build import LIB
 
 MAX_L = 64
 MAX_K = 128
-BINNING = {"equi-depth": 0, "equi-width": 1}
+BINNING = {"equi-depth": 0, "equi-width": 1, "isax": 2}
 
 
 class SofaError(RuntimeError):
@@ -33,7 +33,7 @@ class sofa_model(C.Structure):
         e = np.ctypeslib.as_array(self.edges).reshape(MAX_L, 255)[:l, :a - 1].copy()
         return {"n": self.len, "l": l, "a": a, "best_pos": np.array(self.best_pos[:l], dtype=np.int64),
                 "weights": np.array(self.weights[:l]), "edges": e,
-                "binning": "equi-depth" if self.binning == 0 else "equi-width"}
+                "binning": {0: "equi-depth", 1: "equi-width", 2: "isax"}[self.binning]}
 
     @classmethod
     def from_dict(cls, m: dict) -> "sofa_model":

@@ -87,6 +87,13 @@ def test_build_rejects_bad_opts(L):
     o.model = ctypes.pointer(m)
     assert L.sofa_build(None, 0, 256, 16, 256, ctypes.byref(o), None, ctypes.byref(h)) == -1
     assert "disagrees" in sofa.sofa_last_error()
+    o = sofa.sofa_default_opts()
+    o.binning = sofa.BINNING["isax"]  # iSAX segments need n % l == 0
+    assert L.sofa_build(ctypes.c_void_p(16), 10, 248, 16, 256, ctypes.byref(o), None, ctypes.byref(h)) == -1
+    assert "iSAX" in sofa.sofa_last_error()
+    o.binning = 7
+    assert L.sofa_build(ctypes.c_void_p(16), 10, 256, 16, 256, ctypes.byref(o), None, ctypes.byref(h)) == -1
+    assert "binning" in sofa.sofa_last_error()
 
 
 def test_knn_and_merge_reject_bad_args(L):

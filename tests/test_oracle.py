@@ -300,3 +300,63 @@ def test_sample_indices():
     s = O.sample_indices(100, 7)
     assert list(s) == [0, 14, 28, 42, 57, 71, 85]
     assert len(np.unique(O.sample_indices(10_000_000, 100_000))) == 100_000
+
+
+# ------------------------------------------------------------------ iSAX baseline, SURVEY 8(f) f4
+@pytest.mark.parametrize("key", ["isax_breakpoints_a4", "isax_breakpoints_a2"])
+def test_isax_breakpoints_golden(key):
+    g = GOLD[key]
+    np.testing.assert_allclose(O.isax_breakpoints(g["a"]), g["expected"], atol=g["abs_tol"])
+
+
+@pytest.mark.parametrize("a", [4, 16, 256])
+def test_isax_breakpoints_equal_depth_and_symmetric(a):
+    b = O.isax_breakpoints(a)
+    assert np.all(np.diff(b) > 0)
+    np.testing.assert_allclose(b, -b[::-1], atol=1e-9)
+    # equal depth under N(0,1): each bin holds 1/a of a large normal sample (Monte Carlo, 4 sigma)
+    z = np.random.default_rng(a).normal(size=400_000)
+    counts = np.bincount(np.searchsorted(b, z, side="right"), minlength=a) / z.size
+    assert np.all(np.abs(counts - 1 / a) < 4 * np.sqrt(1 / a / z.size) + 1e-12)
+
+
+@pytest.mark.parametrize("key", ["paa_two_segments", "paa_alternating_flat"])
+def test_paa_golden(key):
+    g = GOLD[key]
+    np.testing.assert_allclose(O.paa(np.array(g["x"]), g["l"])[0], g["expected"], atol=1e-15)
+
+
+def test_isax_mindist_lower_bounds_ed_and_own_word_is_zero():
+    """n/l * sum mind^2 <= ED^2 (PAA contraction + mind <= |paa difference|) on >= 10k pairs"""
+    x = _rw(2500, 128, 31)
+    m = O.isax_model(128, 16, 256)
+    words = O.sfa_words(x, m)
+    xh, _, _, _ = O.znorm(x)
+    q = _rw(6, 128, 32)
+    qh, _, _, _ = O.znorm(q)
+    qp = O.project(q, m)
+    for i in range(q.shape[0]):
+        assert np.all(O.lb_word(qp[i], words, m) <= O.sq_dists_direct(xh, qh[i]) * (1 + 1e-12) + 1e-9)
+    own = O.project(x[:40], m)
+    for i in range(40):
+        assert O.lb_word(own[i], words[i:i + 1], m)[0] == 0.0
+    # PAA contraction itself: (n/l) |paa(x) - paa(q)|^2 <= |x - q|^2
+    px, pq = O.paa(xh, 16), O.paa(qh, 16)
+    assert np.all(8.0 * ((px - pq[0]) ** 2).sum(axis=1) <= O.sq_dists_direct(xh, qh[0]) + 1e-9)
+
+
+def test_isax_flat_on_high_frequency_sfa_is_not():
+    """Fig. 1: on high-frequency series the PAA is nearly flat, so the iSAX bound is far
+    looser than SFA's (mean TLB), the paper's motivation for learned summaries"""
+    x = _hf(1500, 256, 41)
+    q = _hf(6, 256, 42)
+    xh, _, _, _ = O.znorm(x)
+    qh, _, _, _ = O.znorm(q)
+    sfa = O.learn_model(x, 16, 256)
+    isx = O.isax_model(256, 16, 256)
+    tlb = {}
+    for name, m in (("sfa", sfa), ("isax", isx)):
+        words, qp = O.sfa_words(x, m), O.project(q, m)
+        r = [np.sqrt(O.lb_word(qp[i], words, m) / O.sq_dists_direct(xh, qh[i])).mean() for i in range(6)]
+        tlb[name] = float(np.mean(r))
+    assert tlb["isax"] < 0.1 and tlb["sfa"] > 2 * tlb["isax"], tlb
