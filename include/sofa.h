@@ -182,6 +182,15 @@ int sofa_merge_topk(const float* dist_dev, const int64_t* idx_dev, int32_t parts
  * out_host (q x 20).  Errors: EINVAL if no such trace. */
 int sofa_knn_trace(const sofa_index* ix, int64_t* out_host, int32_t q);
 
+/* Lower-bound evaluation (TLB): for each of q queries and m index rows at
+ * sorted positions floor(j*n/m), j < m, the squared SFA (or iSAX) lower bound from the query's
+ * float32 table (entries rounded down, no early abandoning: Sum_j w_j mind_j^2) and
+ * the exact squared z-ED (the refine's arithmetic).  TLB = sqrt(lb2 / ed2).
+ *   queries_dev: q x len float32.  out_lb2_dev, out_ed2_dev: q x m float32.  out_rows_dev: m int64
+ *   (global row index of column j).  All device pointers.  Errors: EINVAL, ECUDA. */
+int sofa_lower_bounds(sofa_index* ix, const float* queries_dev, int32_t q, int64_t m, float* out_lb2_dev,
+                      float* out_ed2_dev, int64_t* out_rows_dev, void* cuda_stream);
+
 /* Copy the index's model to *out (host). */
 int sofa_get_model(const sofa_index* ix, sofa_model* out);
 

@@ -261,7 +261,8 @@ int learn_model_dev(const float* sample, int64_t S, int len, int l, int a, int b
                     cudaStream_t st, sofa_model* out);
 int isax_model(int len, int l, int a, sofa_model* out);
 int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
-                 cudaStream_t st, bool scan = false);
+                 cudaStream_t st, bool scan = false, int64_t lb_m = 0, float* lb_out = nullptr,
+                 float* ed_out = nullptr, int64_t* lb_rows = nullptr);
 // batch-level dense decision (f1): run the tensor-core pass iff the flagged queries' estimated sparse
 // refines add up to at least one full pass over the shard's rows
 inline int64_t dense_batch_rows(const sofa_index* ix) { return ix->n > 0 ? ix->n : 1; }

@@ -85,7 +85,10 @@ struct QArgs {
   int64_t dense_min;
   int64_t dense_rows;  // batch decision: dense pass iff the flagged queries' estimated refines >= this
   int dense_force;     // dense_permille >= 1000: every query with a surviving leaf goes dense (tests)
-  int mode;            // 0: front, 1: scan
+  int mode;            // 0: front, 1: scan, 2: lower-bound evaluation (sofa_lower_bounds)
+  int64_t lb_m;        // mode 2: rows evaluated per query
+  float *lb_out, *ed_out;
+  int64_t* lb_rows;
   int front_batches;   // word batches of LB-ordered leaves the front scans itself per query
   QState* qs;          // q
   float* q_T;          // q x LT x 256 word-LB tables
@@ -846,6 +849,29 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
       s_Thi[e] = thi;
     }
     __syncthreads();
+    if (A.mode == 2) {
+      // lower-bound evaluation (TLB): for rows at sorted positions floor(j n / m), the squared
+      // word LB from this query's table (no abandoning) and the exact squared z-ED
+      for (int64_t j = warp; j < A.lb_m; j += kThreads / 32) {
+        const int64_t pos = j * A.n / A.lb_m;
+        const float* rows[1] = {A.series + (int64_t)A.perm[pos] * len};
+        const float2 st[1] = {A.stats[pos]};
+        const bool on[1] = {true};
+        float d2[1];
+        bool ab[1];
+        ed_warp_multi<NF, 1>(rows, st, on, s_qh4, nf4, INFINITY, d2, ab);
+        if (lane == 0) {
+          uint4 wr[LT / 16];
+#pragma unroll
+          for (int c = 0; c < LT / 16; ++c) wr[c] = ld_stream_u4(A.words + pos * A.WS + 16 * c);
+          A.lb_out[(int64_t)qi * A.lb_m + j] = word_lb<LT>(wr, s_T, INFINITY);
+          A.ed_out[(int64_t)qi * A.lb_m + j] = d2[0];
+          if (qi == 0) A.lb_rows[j] = A.goff + A.perm[pos];
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     // ---------------------------------------------------------------- a6: seed block
     const uint64_t key = word_key(s_qw, l, 31 - __clz(a));
     int64_t lo = 0, hi = A.nb;
@@ -1179,6 +1205,8 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
     }
     SOFA_CK(cudaMemsetAsync(ix->qcounter, 0, 16 * sizeof(int), st));
     SOFA_CK(cudaMemsetAsync(ix->rank_count, 0, (size_t)2 * ix->rank_cap * 4, st));
+  } else if (A.mode == 2) {
+    SOFA_CK(cudaMemsetAsync(ix->qcounter, 0, 16 * sizeof(int), st));
   }
   A.rank_count = reinterpret_cast<int*>(ix->rank_count);
   A.rank_cap = (int)ix->rank_cap;
@@ -1193,9 +1221,13 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
 }
 
 int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
-                 cudaStream_t st, bool scan) {
+                 cudaStream_t st, bool scan, int64_t lb_m, float* lb_out, float* ed_out, int64_t* lb_rows) {
   QArgs A{};
-  A.mode = scan ? 1 : 0;
+  A.mode = lb_m > 0 ? 2 : (scan ? 1 : 0);
+  A.lb_m = lb_m;
+  A.lb_out = lb_out;
+  A.ed_out = ed_out;
+  A.lb_rows = lb_rows;
   A.front_batches = 64;
   if (const char* e = getenv("SOFA_FRONT_BATCHES")) A.front_batches = atoi(e) > 0 ? atoi(e) : 1;  // tuning knob
   A.series = ix->series;

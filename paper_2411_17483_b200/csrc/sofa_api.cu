@@ -440,6 +440,19 @@ int sofa_merge_topk(const float* dist_dev, const int64_t* idx_dev, int32_t parts
   return launch_merge(dist_dev, idx_dev, parts, q, k, out_dist_dev, out_idx_dev, (cudaStream_t)cuda_stream);
 }
 
+int sofa_lower_bounds(sofa_index* ix, const float* queries_dev, int32_t q, int64_t m, float* out_lb2_dev,
+                      float* out_ed2_dev, int64_t* out_rows_dev, void* cuda_stream) {
+  g_err.clear();
+  if (!ix || !queries_dev || !out_lb2_dev || !out_ed2_dev || !out_rows_dev) return fail(SOFA_EINVAL, "NULL pointer");
+  if (q < 1 || m < 1 || m > ix->n) return fail(SOFA_EINVAL, "need q >= 1 and 1 <= m <= n");
+  const bool keep = ix->trace_on;
+  ix->trace_on = 0;
+  const int rc = launch_query(ix, queries_dev, q, 1, nullptr, nullptr, nullptr, (cudaStream_t)cuda_stream, false, m,
+                              out_lb2_dev, out_ed2_dev, out_rows_dev);
+  ix->trace_on = keep;
+  return rc;
+}
+
 int sofa_knn_trace(const sofa_index* ix, int64_t* out_host, int32_t q) {
   if (!ix || !out_host) return fail(SOFA_EINVAL, "NULL pointer");
   if (!ix->trace || q != ix->trace_q) return fail(SOFA_EINVAL, "no trace for this q (call sofa_knn with stats first)");

@@ -60,6 +60,16 @@ class SofaIndex:
         S.sofa_knn_host(self.handle, queries, q, k, out[0], out[1], None, stream)
         return out
 
+    def lower_bounds(self, queries: torch.Tensor, m: int, stream=None):
+        """(lb2, ed2, rows): squared lower bounds and exact squared z-ED of each query against m index
+        rows (sorted positions floor(j n / m)); TLB = sqrt(lb2 / ed2)."""
+        q = queries.shape[0]
+        lb2 = torch.empty(q, m, dtype=torch.float32, device=queries.device)
+        ed2 = torch.empty(q, m, dtype=torch.float32, device=queries.device)
+        rows = torch.empty(m, dtype=torch.int64, device=queries.device)
+        S.sofa_lower_bounds(self.handle, queries.contiguous(), q, m, lb2, ed2, rows, stream)
+        return lb2, ed2, rows
+
     # -------------------------------------------------------------------------------- introspection
     @property
     def model(self) -> dict:

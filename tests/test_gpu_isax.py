@@ -58,3 +58,30 @@ def test_sfa_prunes_better_than_isax_on_high_frequency():
     assert torch.equal(i1, i2) and torch.equal(d1, d2)  # same exact answer
     N, Q = w.n_series, w.n_queries
     assert s1["refined"] < 0.01 * N * Q and 5 * s1["refined"] < s2["refined"], (s1["refined"], s2["refined"])
+
+
+@pytest.mark.parametrize("binning", ["equi-depth", "equi-width", "isax"])
+def test_lower_bounds_entry_matches_oracle(binning):
+    """sofa_lower_bounds (TLB): squared LB from the float32 tables (rounded down) and exact
+    squared z-ED, against the oracle on the same (query, row) pairs and the index's own words"""
+    w = datagen.scaled(datagen.WORKLOADS["cfg1"], 30_000, 12)
+    x, q = _data(w)
+    ix = SofaIndex(x, sample_size=3000, binning=binning)
+    m = 3000
+    lb2, ed2, rows = ix.lower_bounds(q, m)
+    torch.cuda.synchronize()
+    model = ix.model if binning != "isax" else O.isax_model(w.length, 16, 256)
+    words = ix.export()["words"].cpu().numpy()[(np.arange(m) * w.n_series) // m, :16].astype(np.int64)
+    xn, qn = x.cpu().numpy(), q.cpu().numpy()
+    rn = rows.cpu().numpy()
+    assert np.array_equal(np.sort(rn), np.unique(rn))  # m distinct rows
+    xh, _, _, _ = O.znorm(xn[rn])
+    qh, _, _, _ = O.znorm(qn)
+    qp = O.project(qn, model)
+    for i in range(q.shape[0]):
+        lo = O.lb_word(qp[i], words, model)
+        eo = O.sq_dists_direct(xh, qh[i])
+        np.testing.assert_allclose(ed2[i].cpu().numpy(), eo, rtol=1e-4, atol=1e-5)
+        g = lb2[i].cpu().numpy().astype(np.float64)
+        assert np.all(g <= lo * (1 + 1e-5) + 1e-6) and np.all(g >= lo * (1 - 1e-4) - 1e-5)
+        assert np.all(g <= eo * (1 + 1e-4) + 1e-5)  # a lower bound
