@@ -200,10 +200,13 @@ int sofa_get_model(const sofa_index* ix, sofa_model* out);
 int sofa_transform(const float* series_dev, int64_t n, const sofa_model* model, double* out_values_dev,
                    uint8_t* out_words_dev, void* cuda_stream);
 
-/* Index introspection for tests: number of rows / blocks / block size / word stride. */
+/* Index introspection: number of rows / blocks / block size / word stride, and the GPU time of the
+ * build phases (CUDA events on the build stream; the analog of Fig. 7): model (sample +
+ * learning, a2), transform (a1 + a3), sort (a4 key sort), gather + envelopes (a4). */
 typedef struct {
   int64_t n, n_blocks, global_offset, global_n;
   int32_t len, l, alphabet, block_size, word_stride;
+  double build_ms[4];
 } sofa_index_info;
 int sofa_get_info(const sofa_index* ix, sofa_index_info* out);
 

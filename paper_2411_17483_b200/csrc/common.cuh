@@ -215,6 +215,7 @@ struct sofa_index {
   float2* stats = nullptr;        // n, sorted order: (mu, 1/sigma)
   float2* stats_orig = nullptr;   // n, original row order (dense path)
   int32_t dense_permille = 100;   // dense path when >= this many permille of blocks survive (0: off)
+  double build_ms[4] = {};        // model, transform, sort, gather + envelopes (CUDA events)
   DenseScratch dense;
   int32_t* perm = nullptr;        // n: sorted position -> local row
   uint8_t* env = nullptr;         // nb x 2 x WS

@@ -487,10 +487,6 @@ __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd,
       s_have = have;
       if (have) {  // quick reject: a sorted chunk whose first leaf's LB is above the query's BSF
         volatile QState* h = &A.qs[s_task.q];
-        // a dense candidate reached the scan with only its take-round BSF: let its lowest-LB chunk
-        // (rank 0, dispatched before any other rank) tighten the BSF before the others start
-        if ((s_task.cnt_flags & kTaskDense) && s_task.rank > 0)
-          while (h->done < 1) __nanosleep(500);
         const float thr = thr_of(h->bsf);
         S.take = (s_task.cnt_flags & kTaskSorted) && lb_of(A.pool[s_task.off]) > thr;
       }

@@ -207,6 +207,18 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
     return code;
   };
 
+  // build-phase timing (Fig. 7 analog): CUDA events on the build stream
+  struct Events {
+    cudaEvent_t e[5] = {};
+    Events() {
+      for (auto& x : e) cudaEventCreate(&x);
+    }
+    ~Events() {
+      for (auto& x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } ev;
+  cudaEventRecord(ev.e[0], st);
   // ---- a2: model
   if (opts.model) {
     const sofa_model& m = *opts.model;
@@ -236,6 +248,7 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
     if (rc) return bail(rc);
   }
   if ((rc = upload_model(ix->model, len, ix, st))) return bail(rc);
+  cudaEventRecord(ev.e[1], st);
   const int WS = ix->WS, B = ix->B;
   ix->nb = (n + B - 1) / B;
   if (cudaMalloc(&ix->qcounter, 64) != cudaSuccess || cudaMalloc(&ix->dstats, 32 * 8) != cudaSuccess)
@@ -291,6 +304,7 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
     freeall();
     return bail(rc);
   }
+  cudaEventRecord(ev.e[2], st);
   // ---- a4: sort by key (stable: equal keys keep row order), gather, envelopes
   k_iota<<<148 * 8, 256, 0, st>>>(iota, n);
   g_launches.fetch_add(1);
@@ -299,6 +313,7 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
   BCK(cudaMalloc(&tmp, tb + 16));
   BCK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys_u, keys_s, iota, ix->perm, (int64_t)n, 0, 64, st));
   g_launches.fetch_add(1);
+  cudaEventRecord(ev.e[3], st);
   if ((rc = launch_gather(words_u, stats_u, ix->perm, n, WS, ix->words, ix->stats, st)) ||
       (rc = launch_envelopes(ix->words, n, B, WS, keys_s, ix->env, ix->bkey, st))) {
     freeall();
@@ -310,8 +325,14 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
       freeall();
       return bail(rc);
     }
+  cudaEventRecord(ev.e[4], st);
   BCK(cudaStreamSynchronize(st));
 #undef BCK
+  for (int i = 0; i < 4; ++i) {  // model, transform, sort, gather + envelopes
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev.e[i], ev.e[i + 1]);
+    ix->build_ms[i] = ms;
+  }
   freeall();
   *out = ix;
   return SOFA_OK;
@@ -494,6 +515,7 @@ int sofa_get_info(const sofa_index* ix, sofa_index_info* out) {
   out->alphabet = ix->a;
   out->block_size = ix->B;
   out->word_stride = ix->WS;
+  for (int i = 0; i < 4; ++i) out->build_ms[i] = ix->build_ms[i];
   return SOFA_OK;
 }
 

@@ -82,7 +82,9 @@ class SofaIndex:
     @property
     def info(self) -> dict:
         i = S.sofa_get_info(self.handle)
-        return {f: int(getattr(i, f)) for f, _ in i._fields_}
+        d = {f: int(getattr(i, f)) for f, _ in i._fields_ if f != "build_ms"}
+        d["build_ms"] = dict(zip(("model", "transform", "sort", "gather_envelopes"), map(float, i.build_ms)))
+        return d
 
     def export(self) -> dict:
         inf = self.info

@@ -72,7 +72,7 @@ class sofa_knn_stats(C.Structure):
 class sofa_index_info(C.Structure):
     _fields_ = [("n", C.c_int64), ("n_blocks", C.c_int64), ("global_offset", C.c_int64), ("global_n", C.c_int64),
                 ("len", C.c_int32), ("l", C.c_int32), ("alphabet", C.c_int32), ("block_size", C.c_int32),
-                ("word_stride", C.c_int32)]
+                ("word_stride", C.c_int32), ("build_ms", C.c_double * 4)]
 
 
 _LIB = None
