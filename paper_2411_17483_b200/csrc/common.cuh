@@ -167,14 +167,38 @@ __device__ __forceinline__ int bin_of(const E* __restrict__ e, double v) {
 // gives the fewest surviving blocks).  Only the order of blocks depends on it, never a result.
 __device__ __forceinline__ uint64_t word_key(const uint8_t* w, int l, int a_bits) {
   const int P = l < 16 ? l : 16;
+  // symbols 4i..4i+3 normalised to 8 bits in v[i], position 4i in the most significant byte
+  uint32_t v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int p = 4 * i + b;
+      const uint32_t s = p < P ? ((uint32_t)w[p] << (8 - a_bits)) & 0xffu : 0u;
+      x |= s << (24 - 8 * b);
+    }
+    v[i] = x;
+  }
+  // round r: the r-th 2-bit digit (MSB first) of every symbol, packed position-major into 32 bits
+  // with byte-parallel masks; the first 2P bits hold positions 0..P-1
   uint64_t key = 0;
   int nbits = 0;
-  for (int r = 0; r < 4 && nbits < 64; ++r)
-    for (int p = 0; p < P && nbits < 64; ++p) {
-      uint32_t s8 = ((uint32_t)w[p] << (8 - a_bits)) & 0xffu;
-      key = (key << 2) | ((s8 >> (6 - 2 * r)) & 3u);
-      nbits += 2;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    if (nbits >= 64) break;
+    uint32_t packed = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t m = (v[i] >> (6 - 2 * r)) & 0x03030303u;
+      packed = (packed << 8) | ((m >> 18) & 0xC0u) | ((m >> 12) & 0x30u) | ((m >> 6) & 0x0Cu) | (m & 0x03u);
     }
+    const int bits = 2 * P;
+    const int take = bits < 64 - nbits ? bits : 64 - nbits;
+    const uint64_t grp = packed >> (32 - bits);
+    key = (key << take) | (grp >> (bits - take));
+    nbits += take;
+  }
   return nbits < 64 ? key << (64 - nbits) : key;
 }
 
