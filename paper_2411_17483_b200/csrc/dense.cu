@@ -41,6 +41,7 @@ constexpr int DA_BYTES = DM * DKC * 4;  // 16 KB
 constexpr int DB_BYTES = DN * DKC * 4;  // 32 KB
 constexpr int D_THREADS = 320;          // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2..9 epilogue
 constexpr int D_UBK = SOFA_MAX_K;       // k-th-smallest UB tracking (local memory; updates are rare)
+constexpr int D_AHEAD_CHUNKS = 64;      // K-chunks a CTA may run ahead of the others reading its series tiles
 constexpr size_t D_SMEM = 1024 + DSTAGES * (DA_BYTES + DB_BYTES) + 2 * DN * 8 + 64 + 256;
 
 // ------------------------------------------------------------------------------- PTX helpers
@@ -122,6 +123,7 @@ struct DenseArgs {
   int* overflow;  // per slot flag
   int* ovf_list;
   int* ovf_count;
+  int* progress;  // per CTA: items whose loads are issued (zeroed per call)
 };
 
 __device__ __forceinline__ void emit_candidate(const DenseArgs& A, bool pass, int slot, uint32_t row) {
@@ -225,7 +227,27 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       uint32_t phase = 0;
       int m;
       int64_t t;
-      for (int64_t j = 0; dense_item(j, mt, A.n_tiles, m, t); ++j) {
+      // the CTAs that read the same series tiles (one per query tile) stay within a few items of each
+      // other, so a tile fetched from HBM by one of them is still in L2 for the others
+      const int64_t G = gridDim.x, b = blockIdx.x;
+      const bool grouped = mt > 1 && mt <= G && b < (G / mt) * mt;
+      const int64_t g0 = grouped ? (b / mt) * mt : 0;
+      volatile int* prog = A.progress;
+      // slack in items: about D_AHEAD_CHUNKS K-chunks (short items get a wider window)
+      const int64_t ahead = A.KC >= D_AHEAD_CHUNKS / 2 ? 2 : D_AHEAD_CHUNKS / A.KC;
+      int64_t j = 0;
+      for (; dense_item(j, mt, A.n_tiles, m, t); ++j) {
+        if (grouped && j > ahead && j % (ahead / 2 > 0 ? ahead / 2 : 1) == 0) {
+          for (;;) {  // all members' progress loaded together, then compared
+            int lo = 0x7fffffff;
+            for (int64_t o = 0; o < mt; ++o) {
+              const int p = prog[g0 + o];
+              lo = p < lo ? p : lo;
+            }
+            if (lo >= j - ahead) break;
+            __nanosleep(128);
+          }
+        }
         for (int kc = 0; kc < A.KC; ++kc) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], DA_BYTES + DB_BYTES);
@@ -236,7 +258,9 @@ __global__ void __launch_bounds__(D_THREADS, 1)
             phase ^= 1;
           }
         }
+        prog[b] = (int)(j + 1);  // items whose loads this CTA has issued
       }
+      prog[b] = 0x7fffffff;  // done: never holds the group back
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer (one thread)
@@ -363,10 +387,15 @@ __global__ void __launch_bounds__(D_THREADS, 1)
             }
           }
         }
-        if (__any_sync(FULL, amin <= thr_e)) {
+        if (__any_sync(FULL, amin <= thr_e)) {  // rare: emit this chunk's candidates (compact code)
+          uint32_t pass = 0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            emit_candidate(A, __uint_as_float(cur[j]) <= thr_e, slot, (uint32_t)(t * DN + col0 + j));
+          for (int j = 0; j < 32; ++j) pass |= (__uint_as_float(cur[j]) <= thr_e ? 1u : 0u) << j;
+          while (__any_sync(FULL, pass != 0)) {
+            const int j = pass ? __ffs(pass) - 1 : 0;
+            emit_candidate(A, pass != 0, slot, (uint32_t)(t * DN + col0 + j));
+            pass &= pass - 1;
+          }
         }
         if constexpr (KONE) ubk = fminf(ubk, amin + eps);
         thr = fminf(thr, fmaxf(ubk, 0.f));
@@ -580,6 +609,7 @@ int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stat
   A.overflow = D.overflow;
   A.ovf_list = D.ovf_list;
   A.ovf_count = D.counters + 1;
+  A.progress = D.counters + 64;
   auto screen = k == 1 ? k_dense_screen<true> : k_dense_screen<false>;
   static int cached_dev[2] = {-1, -1}, sms = 148;
   if (cached_dev[k == 1] != ix->device) {
@@ -657,7 +687,7 @@ int ensure_dense_scratch(sofa_index* ix, int q, int k) {
   SOFA_CK(cudaMalloc(&D.overflow, (size_t)q * 4));
   SOFA_CK(cudaMalloc(&D.ovf_list, (size_t)q * 4));
   SOFA_CK(cudaMalloc(&D.cand, (size_t)D.cand_cap * 8));
-  SOFA_CK(cudaMalloc(&D.counters, 64));
+  SOFA_CK(cudaMalloc(&D.counters, 64 + 1024 * 4));  // counters, then per-CTA progress
   return SOFA_OK;
 }
 

@@ -360,7 +360,7 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
   const bool dense = ix->n > 0 && ix->dense_permille > 0;
   if (dense) {
     if ((rc = ensure_dense_scratch(ix, q, k))) return rc;
-    SOFA_CK(cudaMemsetAsync(ix->dense.counters, 0, 64, st));
+    SOFA_CK(cudaMemsetAsync(ix->dense.counters, 0, 64 + 1024 * 4, st));
   }
   // with stats: CUDA events on `st` around each launch group (front, dense pass, scan)
   cudaEvent_t ev[4] = {};
