@@ -154,7 +154,8 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
  * cannot prune is flagged for (2) the dense pass (tensor-core TF32 screen with a proven error
  * bound + exact refine) if the flagged queries justify a full pass; (3) the scan
  * pass: every CTA pulls tasks of any query (a7 + a8 against the query's shared top-k); the CTA
- * finishing a query's last task writes its result.
+ * finishing a query's last task writes its result.  Batches larger than 1024 queries run as
+ * consecutive sub-batches on the same stream (the scan pool holds one leaf list per query).
  *   queries_dev: q x len float32 device (raw; z-normalised inside).
  *   bsf_init_dev: nullable, q floats: an upper bound on each query's k-th squared distance
  *   (e.g. from another shard) used to prune; results above it may be absent (padding).

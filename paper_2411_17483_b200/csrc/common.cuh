@@ -13,7 +13,8 @@
 namespace sofa {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kThreads = 256;  // every kernel of the hot path runs 8 warps per CTA
+constexpr int kThreads = 256;     // every kernel of the hot path runs 8 warps per CTA
+constexpr int kQueryBatch = 1024;  // sofa_knn runs larger batches as consecutive sub-batches
 
 extern std::atomic<int64_t> g_launches;
 void set_error(const std::string& msg);
@@ -263,6 +264,7 @@ struct sofa_index {
   long long* trace = nullptr;  // per-query trace (filled when stats are requested)
   int64_t trace_cap = 0;
   int trace_on = 0;
+  int64_t trace_off = 0;  // first query row of the current sub-batch in the trace
   int32_t trace_q = 0;
   // host-path staging
   float* hq_dev = nullptr;

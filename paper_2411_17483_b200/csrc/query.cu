@@ -1255,7 +1255,7 @@ int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_
   A.goff = ix->global_offset;
   A.qcounter = ix->qcounter;
   A.dstats = ix->dstats;
-  A.trace = ix->trace_on ? ix->trace : nullptr;
+  A.trace = ix->trace_on ? ix->trace + ix->trace_off * SOFA_TRACE_FIELDS : nullptr;
   if (ix->dense_permille > 0 && ix->dense.q_cap >= q) {
     const DenseScratch& D = ix->dense;
     A.dense_min = (ix->nb * (ix->dense_permille < 1000 ? ix->dense_permille : 0) + 999) / 1000;

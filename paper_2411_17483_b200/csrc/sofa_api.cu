@@ -358,37 +358,55 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
   if (stats) ix->trace_q = q;
   int rc;
   const bool dense = ix->n > 0 && ix->dense_permille > 0;
-  if (dense) {
-    if ((rc = ensure_dense_scratch(ix, q, k))) return rc;
-    SOFA_CK(cudaMemsetAsync(ix->dense.counters, 0, 64 + 1024 * 4, st));
-  }
+  // large batches run as consecutive sub-batches of kQueryBatch queries on the same stream (the scan
+  // pool holds one leaf list per query: q x ceil(n/B) entries)
+  const int qb_max = q < kQueryBatch ? q : kQueryBatch;
+  if (dense && (rc = ensure_dense_scratch(ix, qb_max, k))) return rc;
   // with stats: CUDA events on `st` around each launch group (front, dense pass, scan)
   cudaEvent_t ev[4] = {};
   if (stats)
     for (auto& e : ev) SOFA_CK(cudaEventCreate(&e));
-  if (stats) SOFA_CK(cudaEventRecord(ev[0], st));
-  if (ix->n == 0) {
-    rc = launch_fill_pad(out_dist_dev, out_idx_dev, (int64_t)q * k, st);
-    if (stats) {
-      cudaEventRecord(ev[1], st);
-      cudaEventRecord(ev[2], st);
+  double kms[3] = {0, 0, 0};
+  rc = SOFA_OK;
+  for (int q0 = 0; q0 < q && !rc; q0 += qb_max) {
+    const int qb = q - q0 < qb_max ? q - q0 : qb_max;
+    const float* Qb = queries_dev + (int64_t)q0 * ix->len;
+    const float* Bb = bsf_init_dev ? bsf_init_dev + q0 : nullptr;
+    float* Db = out_dist_dev + (int64_t)q0 * k;
+    int64_t* Ib = out_idx_dev + (int64_t)q0 * k;
+    ix->trace_off = q0;
+    if (dense) SOFA_CK(cudaMemsetAsync(ix->dense.counters, 0, 64 + 1024 * 4, st));
+    if (stats) cudaEventRecord(ev[0], st);
+    if (ix->n == 0) {
+      rc = launch_fill_pad(Db, Ib, (int64_t)qb * k, st);
+      if (stats) {
+        cudaEventRecord(ev[1], st);
+        cudaEventRecord(ev[2], st);
+      }
+    } else {
+      // front (per query) -> dense pass for flagged queries if the batch warrants it -> scan tasks
+      // (every other leaf chunk of every query, spread over all CTAs); the dense and scan kernels read
+      // the batch decision from device counters, so there is no host synchronisation in between
+      rc = launch_query(ix, Qb, qb, k, Bb, Db, Ib, st, false);
+      if (stats) cudaEventRecord(ev[1], st);
+      if (!rc && dense) rc = launch_dense(ix, qb, k, Db, Ib, stats != nullptr, st);
+      if (stats) cudaEventRecord(ev[2], st);
+      if (!rc) rc = launch_query(ix, Qb, qb, k, Bb, Db, Ib, st, true);
     }
-  } else {
-    // front (per query) -> dense pass for flagged queries if the batch warrants it -> scan tasks
-    // (every other leaf chunk of every query, spread over all CTAs); the dense and scan kernels read
-    // the batch decision from device counters, so there is no host synchronisation in between
-    rc = launch_query(ix, queries_dev, q, k, bsf_init_dev, out_dist_dev, out_idx_dev, st, false);
-    if (stats) cudaEventRecord(ev[1], st);
-    if (!rc && dense) rc = launch_dense(ix, q, k, out_dist_dev, out_idx_dev, stats != nullptr, st);
-    if (stats) cudaEventRecord(ev[2], st);
-    if (!rc) rc = launch_query(ix, queries_dev, q, k, bsf_init_dev, out_dist_dev, out_idx_dev, st, true);
+    if (stats) {
+      cudaEventRecord(ev[3], st);
+      cudaEventSynchronize(ev[3]);
+      for (int i = 0; i < 3; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+        kms[i] += ms;
+      }
+    }
   }
-  if (stats) cudaEventRecord(ev[3], st);
-  if (rc) {
-    for (auto& e : ev)
-      if (e) cudaEventDestroy(e);
-    return rc;
-  }
+  ix->trace_off = 0;
+  if (stats)
+    for (auto& e : ev) cudaEventDestroy(e);
+  if (rc) return rc;
   if (stats) {
     unsigned long long h[32] = {};
     SOFA_CK(cudaMemcpyAsync(h, ix->dstats, 32 * 8, cudaMemcpyDeviceToHost, st));
@@ -414,12 +432,7 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
     stats->dense_refined = (int64_t)h[21];
     stats->scan_tasks = (int64_t)h[22];
     stats->scan_queries = (int64_t)h[23];
-    for (int i = 0; i < 3; ++i) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
-      stats->kernel_ms[i] = ms;
-    }
-    for (auto& e : ev) cudaEventDestroy(e);
+    for (int i = 0; i < 3; ++i) stats->kernel_ms[i] = kms[i];
   }
   return SOFA_OK;
 }

@@ -286,3 +286,30 @@ def test_scan_pool_heavy_queries(Q, k):
     do, io = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), k)
     assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, x.cpu().numpy(), q.cpu().numpy())
     assert st["scan_tasks"] > st["scan_queries"] > 0
+
+
+def test_large_batch_runs_in_sub_batches():
+    """q = 2500 > the internal sub-batch (1024): results, stats and the trace cover every query"""
+    from paper_2411_17483_b200 import sofa as S
+    w = datagen.scaled(datagen.WORKLOADS["cfg1"], 40_000, 2500)
+    x, q = _data(w)
+    ix = SofaIndex(x, sample_size=4000)
+    d, i, st = ix.knn(q, 3, stats=True)
+    torch.cuda.synchronize()
+    assert st["queries"] == 2500
+    tr = S.sofa_knn_trace(ix.handle, 2500)
+    assert np.all(tr[:, :4].sum(axis=1) > 0)  # every query's row was written
+    pick = np.r_[0:5, 1020:1030, 2040:2050, 2495:2500]
+    do, io = O.knn_bruteforce(x.cpu().numpy(), q[pick].cpu().numpy(), 3)
+    assert_knn_parity(d[pick].cpu().numpy(), i[pick].cpu().numpy(), do, io, x.cpu().numpy(), q[pick].cpu().numpy())
+    d1, i1 = ix.knn(q[1000:1100].contiguous(), 3)  # a batch straddling the split gives the same rows
+    assert torch.equal(i1, i[1000:1100]) and torch.equal(d1, d[1000:1100])
+
+
+def test_max_k_and_single_query():
+    w = datagen.scaled(datagen.WORKLOADS["cfg4"], 20_000, 1)
+    x, q = _data(w)
+    ix = SofaIndex(x, sample_size=2000)
+    d, i = ix.knn(q, 128)
+    do, io = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), 128)
+    assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, x.cpu().numpy(), q.cpu().numpy())
