@@ -1,26 +1,27 @@
-// a5..a8: the exact k-NN query path as ONE persistent kernel (one CTA of 8 warps per query at a
-// time; CTAs pull queries from an atomic counter so uneven per-query work balances out).
+// a5..a8: the exact k-NN query path.  One persistent kernel, k_query, in three modes:
+//   front (mode 0): one CTA of 8 warps per query at a time (atomic query counter);
+//   scan  (mode 1): every CTA pulls scan tasks (chunks of any query's remaining leaf list);
+//   lower bounds (mode 2): sofa_lower_bounds (TLB evaluation).
 //
-// Per query:
+// Front, per query:
 //   a5  z-norm (shared row_stats, float32 q-hat for the refine, float64 for the projection),
 //       float64 projection onto the l selected positions, then three l x 256 tables in shared
 //       memory, each entry rounded DOWN to float32 (reading 15):
 //         T  [j][s] = w_j * mind_j(q_j, s)^2                   word LB  (d_SFA)
 //         Tlo[j][s] = w_j * max(0, beta_j(s)   - q_j)^2        envelope lower side
 //         Thi[j][s] = w_j * max(0, q_j - beta_j(s+1))^2        envelope upper side
-//   a6  seed: the query's own-key block (MESSI's approximate search) found by a
-//       256-way parallel search over the blocks' first keys, scanned + refined -> BSF0;
-//       then the envelope LB of every block (leaf LB); blocks with LB <= thr are
-//       appended to a per-CTA list and, when <= CAP_B of them survive, bitonic-sorted by LB in
-//       shared memory (MESSI's priority queue: process leaves in ascending LB, stop
-//       at the first whose LB exceeds the BSF).
-//   a7  word LB scan of the listed blocks in batches of CAP_C words: 16-byte word loads, table
-//       gathers in chunks of 8 positions with early abandoning (Alg. 3), survivors
-//       appended to a shared candidate buffer (warp-aggregated atomics).
-//   a8  candidates sorted by LB, refined in waves of 8 (one warp per candidate, float4 row
-//       loads, warp-shuffle reduction, early abandoning per 256-element chunk vs BSF),
-//       top-k kept sorted by (d^2, index); refinement stops at the first candidate whose LB
-//       exceeds the threshold.
+//   a6  seed: the query's own-key block (MESSI's approximate search) found by a 256-way
+//       parallel search over the blocks' first keys, scanned + refined -> BSF0; the envelope tree
+//       descent (leaf LB) -> the surviving leaves; top-M seeding (the 32 lowest word
+//       LBs of the ~64 lowest-LB leaves are refined, SURVEY SIM-6) and a re-filter; the dense-path
+//       decision (dense.cu); then up to a budget of leaves in ascending LB with MESSI's stop rule
+//       (priority queue order), the rest published as scan tasks.
+//   a7+a8  scan_blocks: barrier-free, warp-centric: a warp takes the next leaf, computes its words'
+//       LBs (Alg. 3, chunks of 8 positions with early abandoning) and refines its
+//       candidates in ascending LB, R rows at a time (exact squared z-ED with early abandoning,
+//       P:382), improvements into the top-k sorted by (d^2, index).
+// Scan: a rank-major task pool (every query's lowest-LB chunk first); a chunk whose first leaf LB
+// exceeds the query's BSF is rejected unread; the CTA finishing a query's last task writes it.
 // thr = BSF * (1 + 1e-4) + 1e-5 (squared units): prune only when the float32 lower bound clearly
 // exceeds the float32 k-th best; this absorbs the data-side projection error (reading 15).
 #include <cstdlib>
@@ -37,7 +38,7 @@ constexpr int KMAX = SOFA_MAX_K;
 constexpr int kFan = 16;  // envelope tree fan-out
 
 // Front / scan split.  The front mode of k_query does the per-query steps (a5 tables, a6 seed and
-// envelope descent, the TAKE_F lowest-LB leaves, the dense-path decision) and publishes the rest of
+// envelope descent, top-M seeding, the dense-path decision, a budget of leaves) and publishes the rest of
 // the query's leaf list as scan tasks (chunks of leaves) into a global pool; the scan mode spreads
 // all queries' tasks over all CTAs, so a heavy query no longer sits on one CTA.  A query's top-k
 // lives in its QState while tasks are in flight; the CTA that finishes its last task writes the
@@ -49,13 +50,11 @@ struct QState {
   int tki[SOFA_MAX_K];
 };
 struct ScanTask {
-  int64_t off;  // into the leaf pool
+  int64_t off;    // into the leaf pool
   int q;
-  int cnt_flags;  // leaves | sorted << 30 | dense candidate << 29
-  int rank;       // position in the query's LB-ordered chunk sequence
-  int pad;
+  int cnt_flags;  // leaves | sorted << 30
 };
-constexpr int kTaskSorted = 1 << 30, kTaskDense = 1 << 29, kTaskCnt = (1 << 29) - 1;
+constexpr int kTaskSorted = 1 << 30, kTaskCnt = (1 << 29) - 1;
 
 struct QArgs {
   const float* series;
@@ -153,7 +152,7 @@ __device__ __forceinline__ void warp_append(bool pass, unsigned long long key, u
 }
 
 struct QShared {
-  int qi, cnt, ncand, tkn, b0, take, rem, next, lock, gslot, chunk, ntask, p1, p2;
+  int qi, cnt, tkn, take, rem, next, lock, gslot, chunk, ntask;
   long long off;
   float bsf, bsf_init, thr;
   // per query: 0 blocks_survived, 1 words_scanned, 2 candidates, 3 refined, 4 abandoned, 5 env_nodes,
@@ -438,9 +437,8 @@ __device__ void publish_tasks(const QArgs& A, QShared& S, int q, const unsigned 
     ScanTask t;
     t.off = off + (int64_t)i * CH;
     t.q = q;
-    t.cnt_flags = (n - i * CH < CH ? n - i * CH : CH) | flags | (dense_cand ? kTaskDense : 0);
+    t.cnt_flags = (n - i * CH < CH ? n - i * CH : CH) | flags;
     const int r = r0 + i;
-    t.rank = r;
     if (r < A.rank_cap) tasks[(int64_t)r * A.q + atomicAdd(&rc[r], 1)] = t;
   }
   __syncthreads();
@@ -508,7 +506,6 @@ __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd,
         S.bsf_init = h->bsf_init;
         S.bsf = h->bsf;
         S.thr = thr_of(S.bsf);
-        S.ncand = 0;
         S.next = 0;
         S.lock = 0;
       }
@@ -804,7 +801,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
       }
       if (lane == 0) {
         S.cnt = 0;
-        S.ncand = 0;
         S.tkn = 0;
         S.next = 0;
         S.lock = 0;
