@@ -185,12 +185,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local %= max(1, torch.cuda.device_count())  # one GPU per rank; a 1-GPU box can still run a smoke
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        # NCCL over NVLink; SOFA_DIST_BACKEND=gloo runs the same sharded path with several ranks on one
+        # GPU (a check of the multi-rank code path, not a measurement)
+        backend = os.environ.get("SOFA_DIST_BACKEND", "nccl")
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     lo, hi = datagen.shard_range(w.n_series, rank, world)
 
     # ---------------------------------------------------------------- data (resident in HBM)
@@ -229,7 +233,12 @@ def main():
     for _ in range(a.warmup):
         knn(q)
     torch.cuda.synchronize()
-    _, _, st = index.knn(q, w.k, stats=True)  # pruning statistics of this shard (same work as a step)
+    # pruning statistics of this shard (same work as a step: with N > 1, under the exchanged bound)
+    if world == 1:
+        _, _, st = index.knn(q, w.k, stats=True)
+    else:
+        from paper_2411_17483_b200.distributed import exchange_bound
+        _, _, st = index.knn(q, w.k, bsf_init=exchange_bound(index.knn_seed(q, w.k)), stats=True)
 
     # ---------------------------------------------------------------- timed steps
     times = []

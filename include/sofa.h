@@ -165,6 +165,16 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
 int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, const float* bsf_init_dev,
              float* out_dist_dev, int64_t* out_idx_dev, sofa_knn_stats* stats, void* cuda_stream);
 
+/* Seed bound for sharded search (the optional best-so-far exchange of BASELINE.json's
+ * north_star): per query, the k-th smallest squared z-ED among the rows this index's seed step
+ * refines (the own-key leaf, MESSI's approximate search P:169, and the 32 lowest word LBs of the
+ * lowest-LB leaves), +inf if fewer than k.  The minimum of it over shards bounds the GLOBAL k-th
+ * best, so passing that minimum as `bsf_init` to every shard's sofa_knn prunes shards that do not
+ * hold the neighbours without changing the merged result.
+ *   queries_dev: q x len float32; out_bound_dev: q float32.  Device pointers.  Errors: EINVAL, ECUDA. */
+int sofa_knn_seed(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, float* out_bound_dev,
+                  void* cuda_stream);
+
 /* Same as sofa_knn with HOST buffers: copies the queries host->device, runs the search and
  * copies the results device->host inside the call (end-to-end path).  Synchronous. */
 int sofa_knn_host(sofa_index* ix, const float* queries_host, int32_t q, int32_t k,

@@ -289,7 +289,7 @@ int learn_model_dev(const float* sample, int64_t S, int len, int l, int a, int b
 int isax_model(int len, int l, int a, sofa_model* out);
 int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
                  cudaStream_t st, bool scan = false, int64_t lb_m = 0, float* lb_out = nullptr,
-                 float* ed_out = nullptr, int64_t* lb_rows = nullptr);
+                 float* ed_out = nullptr, int64_t* lb_rows = nullptr, float* seed_out = nullptr);
 // batch-level dense decision (f1): run the tensor-core pass iff the flagged queries' estimated sparse
 // refines add up to at least one full pass over the shard's rows
 inline int64_t dense_batch_rows(const sofa_index* ix) { return ix->n > 0 ? ix->n : 1; }
@@ -298,4 +298,5 @@ int ensure_dense_scratch(sofa_index* ix, int q, int k);
 void free_dense_scratch(sofa_index* ix);
 int launch_merge(const float* d, const int64_t* i, int parts, int q, int k, float* od, int64_t* oi, cudaStream_t st);
 int launch_fill_pad(float* od, int64_t* oi, int64_t cnt, cudaStream_t st);
+int launch_fill_value(float* o, int64_t cnt, float v, cudaStream_t st);
 }  // namespace sofa

@@ -84,7 +84,8 @@ struct QArgs {
   int64_t dense_min;
   int64_t dense_rows;  // batch decision: dense pass iff the flagged queries' estimated refines >= this
   int dense_force;     // dense_permille >= 1000: every query with a surviving leaf goes dense (tests)
-  int mode;            // 0: front, 1: scan, 2: lower-bound evaluation (sofa_lower_bounds)
+  int mode;            // 0: front, 1: scan, 2: lower-bound evaluation (sofa_lower_bounds), 3: seed bound
+  float* seed_out;     // mode 3: per query, the k-th best squared distance of the seeded rows
   int64_t lb_m;        // mode 2: rows evaluated per query
   float *lb_out, *ed_out;
   int64_t* lb_rows;
@@ -922,6 +923,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
     {
       int cnt = S.cnt;
       if (tid == 0) S.st[6] += cnt;
+      if (A.mode == 3 && cnt > 0 && cnt <= TOPM_MIN_LEAVES) {  // seed bound of a short list: top-M over all of it
+        for (int i = tid; i < cnt; i += kThreads) s_blist[i] = gl[i];
+        __syncthreads();
+        seed_topm<LT, NF>(A, S, s_blist, cnt, s_T, s_tkd, s_tki, s_qh4);
+      }
       if (cnt > TOPM_MIN_LEAVES) {
         // top-M seeding over the TOPM_LEAVES lowest-LB leaves (threshold from a sorted strided sample)
         s_samp[tid] = gl[((int64_t)tid * cnt) / kThreads];
@@ -947,6 +953,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
         unsigned long long* t = gl;
         gl = gl2;
         gl2 = t;
+      }
+      if (A.mode == 3) {  // sofa_knn_seed: this shard's bound on the k-th best, nothing else
+        if (tid == 0) A.seed_out[qi] = S.tkn == A.k ? S.bsf : INFINITY;
+        __syncthreads();
+        continue;
       }
       if (tid == 0) {
         s_dense = -1;
@@ -1197,7 +1208,7 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
     }
     SOFA_CK(cudaMemsetAsync(ix->qcounter, 0, 16 * sizeof(int), st));
     SOFA_CK(cudaMemsetAsync(ix->rank_count, 0, (size_t)2 * ix->rank_cap * 4, st));
-  } else if (A.mode == 2) {
+  } else if (A.mode >= 2) {
     SOFA_CK(cudaMemsetAsync(ix->qcounter, 0, 16 * sizeof(int), st));
   }
   A.rank_count = reinterpret_cast<int*>(ix->rank_count);
@@ -1213,9 +1224,11 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
 }
 
 int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
-                 cudaStream_t st, bool scan, int64_t lb_m, float* lb_out, float* ed_out, int64_t* lb_rows) {
+                 cudaStream_t st, bool scan, int64_t lb_m, float* lb_out, float* ed_out, int64_t* lb_rows,
+                 float* seed_out) {
   QArgs A{};
-  A.mode = lb_m > 0 ? 2 : (scan ? 1 : 0);
+  A.mode = seed_out ? 3 : (lb_m > 0 ? 2 : (scan ? 1 : 0));
+  A.seed_out = seed_out;
   A.lb_m = lb_m;
   A.lb_out = lb_out;
   A.ed_out = ed_out;
@@ -1316,6 +1329,17 @@ __global__ void k_merge_topk(const float* __restrict__ d, const int64_t* __restr
 
 int launch_merge(const float* d, const int64_t* i, int parts, int q, int k, float* od, int64_t* oi, cudaStream_t st) {
   k_merge_topk<<<(q + 127) / 128, 128, 0, st>>>(d, i, parts, q, k, od, oi);
+  SOFA_LAUNCHED();
+  return SOFA_OK;
+}
+
+__global__ void k_fill_value(float* o, int64_t cnt, float v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = v;
+}
+
+int launch_fill_value(float* o, int64_t cnt, float v, cudaStream_t st) {
+  k_fill_value<<<(int)((cnt + 255) / 256 < 1024 ? (cnt + 255) / 256 : 1024), 256, 0, st>>>(o, cnt, v);
   SOFA_LAUNCHED();
   return SOFA_OK;
 }

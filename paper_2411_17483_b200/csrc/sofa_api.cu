@@ -487,6 +487,25 @@ int sofa_lower_bounds(sofa_index* ix, const float* queries_dev, int32_t q, int64
   return rc;
 }
 
+int sofa_knn_seed(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, float* out_bound_dev,
+                  void* cuda_stream) {
+  g_err.clear();
+  if (!ix || !queries_dev || !out_bound_dev) return fail(SOFA_EINVAL, "NULL pointer");
+  if (q < 1 || k < 1 || k > SOFA_MAX_K) return fail(SOFA_EINVAL, "need q >= 1 and 1 <= k <= 128");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (ix->n == 0) return launch_fill_value(out_bound_dev, q, INFINITY, st);
+  const bool keep = ix->trace_on;
+  ix->trace_on = 0;
+  int rc = SOFA_OK;
+  for (int q0 = 0; q0 < q && !rc; q0 += kQueryBatch) {
+    const int qb = q - q0 < kQueryBatch ? q - q0 : kQueryBatch;
+    rc = launch_query(ix, queries_dev + (int64_t)q0 * ix->len, qb, k, nullptr, nullptr, nullptr, st, false, 0,
+                      nullptr, nullptr, nullptr, out_bound_dev + q0);
+  }
+  ix->trace_on = keep;
+  return rc;
+}
+
 int sofa_knn_trace(const sofa_index* ix, int64_t* out_host, int32_t q) {
   if (!ix || !out_host) return fail(SOFA_EINVAL, "NULL pointer");
   if (!ix->trace || q != ix->trace_q) return fail(SOFA_EINVAL, "no trace for this q (call sofa_knn with stats first)");

@@ -65,9 +65,22 @@ def allgather_topk(dist_local: torch.Tensor, idx_local: torch.Tensor, group=None
     return torch.stack(dl), torch.stack(il)
 
 
-def sharded_knn(queries, k, local_knn, merge, group=None):
-    """Local k-NN on this rank's shard, all-gather, min-merge (a9)."""
-    d, i = local_knn(queries, k)
+def exchange_bound(bound: torch.Tensor, group=None) -> torch.Tensor:
+    """C3: per query, the minimum over ranks of the local bound on the k-th best squared distance —
+    a bound on the GLOBAL k-th best (the k rows behind any rank's bound are k distinct rows)."""
+    dist.all_reduce(bound, op=dist.ReduceOp.MIN, group=group)
+    return bound
+
+
+def sharded_knn(queries, k, local_knn, merge, group=None, local_seed=None):
+    """Local k-NN on this rank's shard, all-gather, min-merge (a9).  With `local_seed`, the ranks
+    first exchange their seed bounds (C3) and every shard searches under the global one, so a
+    shard that does not hold a query's neighbours prunes almost everything."""
+    if local_seed is not None:
+        bound = exchange_bound(local_seed(queries, k), group)
+        d, i = local_knn(queries, k, bound)
+    else:
+        d, i = local_knn(queries, k)
     D, I = allgather_topk(d, i, group)
     return merge(D, I)
 
@@ -94,6 +107,8 @@ class ShardedSofa:
         self.index = SofaIndex(shard, l=l, alphabet=alphabet, block_size=block_size, model=model,
                                global_offset=global_offset, global_n=global_n)
 
-    def knn(self, queries: torch.Tensor, k: int):
+    def knn(self, queries: torch.Tensor, k: int, exchange_bound: bool = True):
         from .index import merge_topk
-        return sharded_knn(queries, k, self.index.knn, merge_topk, self.group)
+        seed = self.index.knn_seed if exchange_bound else None
+        local = (lambda qs, kk, b=None: self.index.knn(qs, kk, bsf_init=b)) if exchange_bound else self.index.knn
+        return sharded_knn(queries, k, local, merge_topk, self.group, local_seed=seed)

@@ -60,6 +60,14 @@ class SofaIndex:
         S.sofa_knn_host(self.handle, queries, q, k, out[0], out[1], None, stream)
         return out
 
+    def knn_seed(self, queries: torch.Tensor, k: int = 1, stream=None) -> torch.Tensor:
+        """(q,) float32: this index's seed bound on each query's k-th best squared distance (the
+        k-th best of the rows its seed step refines; +inf if fewer).  Sharded search all-reduces
+        the minimum over shards and passes it as `bsf_init` (distributed.ShardedSofa)."""
+        out = torch.empty(queries.shape[0], dtype=torch.float32, device=queries.device)
+        S.sofa_knn_seed(self.handle, queries.contiguous(), queries.shape[0], k, out, stream)
+        return out
+
     def lower_bounds(self, queries: torch.Tensor, m: int, stream=None):
         """(lb2, ed2, rows): squared lower bounds and exact squared z-ED of each query against m index
         rows (sorted positions floor(j n / m)); TLB = sqrt(lb2 / ed2)."""

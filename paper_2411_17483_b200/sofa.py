@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
         L.sofa_get_model.argtypes = [VP, P(sofa_model)]
         L.sofa_knn_trace.argtypes = [VP, VP, I32]
         L.sofa_lower_bounds.argtypes = [VP, VP, I32, I64, VP, VP, VP, VP]
+        L.sofa_knn_seed.argtypes = [VP, VP, I32, I32, VP, VP]
         L.sofa_transform.argtypes = [VP, I64, P(sofa_model), VP, VP, VP]
         L.sofa_get_info.argtypes = [VP, P(sofa_index_info)]
         L.sofa_export_index.argtypes = [VP, VP, VP, VP, VP, VP]
@@ -184,6 +185,10 @@ def sofa_knn_trace(ix, q) -> np.ndarray:
 def sofa_lower_bounds(ix, queries_dev, q, m, out_lb2_dev, out_ed2_dev, out_rows_dev, stream=None):
     _ck(lib().sofa_lower_bounds(ix, _ptr(queries_dev), q, m, _ptr(out_lb2_dev), _ptr(out_ed2_dev),
                                 _ptr(out_rows_dev), _stream(stream)))
+
+
+def sofa_knn_seed(ix, queries_dev, q, k, out_bound_dev, stream=None):
+    _ck(lib().sofa_knn_seed(ix, _ptr(queries_dev), q, k, _ptr(out_bound_dev), _stream(stream)))
 
 
 def sofa_get_model(ix) -> sofa_model:

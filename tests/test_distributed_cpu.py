@@ -51,7 +51,20 @@ def _worker(rank, world, port, q):
 
         d, i = D.sharded_knn(queries, k, local_knn, merge)
         do, io = O.knn_bruteforce(full.numpy(), queries.numpy(), k)
-        q.put((rank, ok_sample, got == b"model-bytes-7", bool(np.array_equal(i.numpy(), io)),
+        # with the seed-bound exchange (C3): each rank's bound = the k-th best of a few of its rows,
+        # the all-reduced minimum bounds the global k-th best; shards drop rows above it
+        def local_seed(qs, kk):
+            ds, _ = O.knn_bruteforce(shard.numpy()[:64], qs.numpy(), kk)
+            return torch.from_numpy((ds[:, -1] ** 2).astype(np.float32))
+
+        def local_knn_bounded(qs, kk, bound):
+            dd, ii = local_knn(qs, kk)
+            drop = dd.double() ** 2 > bound.double()[:, None] * (1 + 1e-6)
+            return torch.where(drop, torch.full_like(dd, float("inf")), dd), torch.where(drop, -1, ii)
+
+        d2, i2 = D.sharded_knn(queries, k, local_knn_bounded, merge, local_seed=local_seed)
+        ok_bound = bool(np.array_equal(i2.numpy(), io))
+        q.put((rank, ok_sample, got == b"model-bytes-7", bool(np.array_equal(i.numpy(), io)) and ok_bound,
                float(np.max(np.abs(d.numpy() - do) / do))))
     finally:
         dist.destroy_process_group()

@@ -313,3 +313,21 @@ def test_max_k_and_single_query():
     d, i = ix.knn(q, 128)
     do, io = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), 128)
     assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, x.cpu().numpy(), q.cpu().numpy())
+
+
+@pytest.mark.parametrize("kind,k", [("cfg2", 1), ("cfg1", 4), ("cfg3", 2)])
+def test_knn_seed_bound_is_a_valid_upper_bound(kind, k):
+    """sofa_knn_seed: per query an upper bound on the k-th best squared distance (the k-th best of
+    real rows); for noisy members it is already the nearest neighbour's distance"""
+    w = datagen.scaled(datagen.WORKLOADS[kind], 60_000, 40)
+    x, q = _data(w)
+    ix = SofaIndex(x, sample_size=6000)
+    b = ix.knn_seed(q, k).cpu().numpy().astype(np.float64)
+    do, _ = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), k)
+    kth2 = do[:, -1] ** 2
+    assert np.all(b >= kth2 * (1 - 1e-4) - 1e-6)
+    if kind == "cfg2":
+        assert np.mean(np.abs(b - kth2) <= 1e-4 * kth2 + 1e-6) > 0.9
+    d1, i1 = ix.knn(q, k)
+    d2, i2 = ix.knn(q, k, bsf_init=torch.from_numpy(b.astype(np.float32)).cuda())
+    assert torch.equal(i1, i2) and torch.equal(d1, d2)
