@@ -1058,7 +1058,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
       const int CH = chunk_blocks<LT>(A.B);
       const int budget = A.front_batches * batch_blocks<LT>(A.B);  // leaves the front scans itself
       if (tid == 0) S.ntask = 0;
-      if (cnt <= CAP_B) {
+      __syncthreads();
+      if (dc) {
+        // a dense candidate's leaves are only needed if the batch skips the dense pass: publish them
+        // as they are (one pass; no ordering work for a list that is usually never scanned)
+        publish_tasks<LT>(A, S, qi, gl, cnt, false, true);
+      } else if (cnt <= CAP_B) {
         for (int i = tid; i < cnt; i += kThreads) s_blist[i] = gl[i];
         __syncthreads();
         bitonic_sort_u64(s_blist, cnt);
