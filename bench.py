@@ -330,6 +330,27 @@ def main():
                "h2d_bytes_per_step": int(w.n_queries * w.length * 4),
                "d2h_bytes_per_step": int(w.n_queries * w.k * 12)}
 
+    # ---------------------------------------------------------------- cpu brute-force scan (UCR Suite-P style)
+    # BASELINE.json north_star: "a multithreaded CPU brute-force scan, timed on the box's host cores in
+    # the same run"; rank 0, N=1; a bounded sample (8 queries over up to 10M rows), extrapolated in N
+    cpu_scan_line = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        import cpu_scan
+        rows = min(w.n_series, 10_000_000 if w.length <= 256 else 2_500_000)
+        xs = x[:rows].cpu().numpy()
+        qs = q[:8].cpu().numpy()
+        stats_h = cpu_scan.row_stats(xs)
+        cpu_scan.knn(xs, stats_h, qs[:1], w.k, threads=cores())  # warm-up (page faults, threads)
+        t0 = time.perf_counter()
+        cpu_scan.knn(xs, stats_h, qs, w.k, threads=cores())
+        dt = time.perf_counter() - t0
+        per_q = dt / len(qs) * (w.n_series / rows)
+        cpu_scan_line = {"value": 1.0 / per_q, "unit": UNIT, "cores": cores(), "kind": "ucr-suite-p-style OpenMP "
+                         "float32 brute force, early abandoning (cpu_scan/)", "seconds": dt,
+                         "sample": f"{len(qs)} queries x first {rows:,} of {w.n_series:,} rows, time extrapolated "
+                                   "linearly in N"}
+        del xs
+
     # ---------------------------------------------------------------- cpu baseline (oracle), rank 0, N=1
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -358,7 +379,7 @@ def main():
             "knn_stats": st,
             "build": {"ms": build_ms, "gb_per_s_series_read": (hi - lo) * w.length * 4 / (build_ms / 1e3) / 1e9},
             "roofline": roofline, "roofline_all": rooflines, "kernel_ms": km,
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+            "cpu_baseline": cpu, "cpu_scan": cpu_scan_line, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
     index.close()
