@@ -89,7 +89,8 @@ struct QArgs {
   int64_t lb_m;        // mode 2: rows evaluated per query
   float *lb_out, *ed_out;
   int64_t* lb_rows;
-  int front_batches;   // word batches of LB-ordered leaves the front scans itself per query
+  int front_batches;  // word batches of LB-ordered leaves the front scans itself per query
+  int rev_rounds;     // scan_blocks: refine rounds per unit before it is deferred to the revisit pass
   QState* qs;          // q
   float* q_T;          // q x LT x 256 word-LB tables
   float* q_hat;        // q x len z-normalised queries
@@ -153,7 +154,7 @@ __device__ __forceinline__ void warp_append(bool pass, unsigned long long key, u
 }
 
 struct QShared {
-  int qi, cnt, tkn, take, rem, next, lock, gslot, chunk, ntask;
+  int qi, cnt, tkn, take, rem, next, lock, gslot, chunk, ntask, nrev;
   long long off;
   float bsf, bsf_init, thr;
   // per query: 0 blocks_survived, 1 words_scanned, 2 candidates, 3 refined, 4 abandoned, 5 env_nodes,
@@ -277,117 +278,152 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
   const int span = B / ppl, wpl = span / 32;
   const int units = cnt * ppl;
   const int nf4 = A.len >> 2;
+  // Pass 0 scans the list; a unit with more candidates than A.rev_rounds x R refines only its lowest
+  // ones now (so the BSF keeps improving) and is queued for pass 1, which rescans it after the whole
+  // list — under a BSF that is by then nearly final — skipping the candidates already refined.
+  constexpr int REV_CAP = 128;
+  __shared__ int s_rev_u[REV_CAP];
+  __shared__ unsigned long long s_rev_k[REV_CAP];
   __syncthreads();
-  if (tid == 0) S.next = 0;
+  if (tid == 0) {
+    S.next = 0;
+    S.nrev = 0;
+  }
   __syncthreads();
   unsigned n_words = 0, n_cand = 0, n_ref = 0, n_ab = 0, n_units = 0, n_leaf = 0;
-  for (;;) {
-    int u = 0;
-    float thr = 0.f;
-    if (lane == 0) {
-      u = atomicAdd(&S.next, 1);
-      thr = *(volatile float*)&S.thr;
-    }
-    u = __shfl_sync(FULL, u, 0);
-    thr = __shfl_sync(FULL, thr, 0);
-    if (u >= units) break;
-    const int e = u / ppl, part = u % ppl;
-    const unsigned long long ent = list[e];
-    if (lb_of(ent) > thr) {
-      if (sorted) break;  // every later leaf has a larger LB
-      continue;
-    }
-    ++n_units;
-    n_leaf += part == 0;
-    const int64_t base = (int64_t)(uint32_t)ent * B + (int64_t)part * span;
-    uint4 wr[WMAX][NC];
-    bool ok[WMAX];
-#pragma unroll
-    for (int i = 0; i < WMAX; ++i) {
-      const int64_t pos = base + i * 32 + lane;
-      ok[i] = i < wpl && pos < A.n;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) wr[i][c] = ok[i] ? ld_stream_u4(A.words + pos * A.WS + 16 * c) : make_uint4(0u, 0u, 0u, 0u);
-    }
-    float lbv[WMAX];
-#pragma unroll
-    for (int i = 0; i < WMAX; ++i) {
-      lbv[i] = ok[i] ? word_lb<LT>(wr[i], s_T, thr) : __int_as_float(0x7fffffff);  // NaN: never <= thr
-      n_words += ok[i];
-      n_cand += lbv[i] <= thr;
-    }
-    for (;;) {  // refine this unit's candidates, R lowest LBs at a time
-      float bsf = 0.f;
+  for (int pass = 0; pass < 2; ++pass) {
+    const int total = pass == 0 ? units : (S.nrev < REV_CAP ? S.nrev : REV_CAP);
+    for (;;) {
+      int idx = 0;
+      float thr = 0.f;
       if (lane == 0) {
+        idx = atomicAdd(&S.next, 1);
         thr = *(volatile float*)&S.thr;
-        bsf = *(volatile float*)&S.bsf;
       }
+      idx = __shfl_sync(FULL, idx, 0);
       thr = __shfl_sync(FULL, thr, 0);
-      bsf = __shfl_sync(FULL, bsf, 0);
-      bool mine = false;
+      if (idx >= total) break;
+      const int u = pass == 0 ? idx : s_rev_u[idx];
+      const unsigned long long done_key = pass == 0 ? 0ull : s_rev_k[idx];  // refined in pass 0: keys <= this
+      const int e = u / ppl, part = u % ppl;
+      const unsigned long long ent = list[e];
+      if (lb_of(ent) > thr) {
+        if (sorted && pass == 0) break;  // every later leaf has a larger LB
+        continue;
+      }
+      if (pass == 0) {
+        ++n_units;
+        n_leaf += part == 0;
+      }
+      const int64_t base = (int64_t)(uint32_t)ent * B + (int64_t)part * span;
+      uint4 wr[WMAX][NC];
+      bool ok[WMAX];
 #pragma unroll
-      for (int i = 0; i < WMAX; ++i) mine |= lbv[i] <= thr;
-      if (!__any_sync(FULL, mine)) break;  // the common case: no candidate left in this unit
-      const float* rows[R];
-      float2 st[R];
-      bool on[R];
-      int oidx[R];
-      bool any = false;
+      for (int i = 0; i < WMAX; ++i) {
+        const int64_t pos = base + i * 32 + lane;
+        ok[i] = i < wpl && pos < A.n;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        unsigned long long best = ~0ull;
+        for (int c = 0; c < NC; ++c) wr[i][c] = ok[i] ? ld_stream_u4(A.words + pos * A.WS + 16 * c) : make_uint4(0u, 0u, 0u, 0u);
+      }
+      float lbv[WMAX];
 #pragma unroll
-        for (int i = 0; i < WMAX; ++i)
-          if (lbv[i] <= thr) {
-            const unsigned long long key = pack(lbv[i], (uint32_t)(i * 32 + lane));
-            best = key < best ? key : best;
-          }
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) {
-          const unsigned long long other = __shfl_xor_sync(FULL, best, o);
-          best = other < best ? other : best;
-        }
-        on[r] = best != ~0ull;
-        oidx[r] = -1;
-        rows[r] = A.series;
-        st[r] = make_float2(0.f, 0.f);
-        if (on[r]) {
-          const int slot = (int)(uint32_t)best;
-#pragma unroll
-          for (int i = 0; i < WMAX; ++i)
-            if (slot == i * 32 + lane) lbv[i] = __int_as_float(0x7fffffff);  // taken
-          const int64_t pos = base + slot;
-          oidx[r] = A.perm[pos];
-          st[r] = A.stats[pos];
-          rows[r] = A.series + (int64_t)oidx[r] * A.len;
-          any = true;
+      for (int i = 0; i < WMAX; ++i) {
+        lbv[i] = ok[i] ? word_lb<LT>(wr[i], s_T, thr) : __int_as_float(0x7fffffff);  // NaN: never <= thr
+        if (pass == 1 && ok[i] && pack(lbv[i], (uint32_t)(i * 32 + lane)) <= done_key)
+          lbv[i] = __int_as_float(0x7fffffff);  // refined in pass 0
+        if (pass == 0) {
+          n_words += ok[i];
+          n_cand += lbv[i] <= thr;
         }
       }
-      if (!any) break;
-      float d2[R];
-      bool ab[R];
-      ed_warp_multi<NF, R>(rows, st, on, s_qh4, nf4, bsf, d2, ab);
-      if (lane == 0) {
+      unsigned long long last_key = 0ull;
+      for (int rounds = 0;; ++rounds) {  // refine this unit's candidates, R lowest LBs at a time
+        float bsf = 0.f;
+        if (lane == 0) {
+          thr = *(volatile float*)&S.thr;
+          bsf = *(volatile float*)&S.bsf;
+        }
+        thr = __shfl_sync(FULL, thr, 0);
+        bsf = __shfl_sync(FULL, bsf, 0);
+        bool mine = false;
+#pragma unroll
+        for (int i = 0; i < WMAX; ++i) mine |= lbv[i] <= thr;
+        if (!__any_sync(FULL, mine)) break;  // the common case: no candidate left in this unit
+        if (pass == 0 && rounds == A.rev_rounds) {  // many candidates: a loose BSF; revisit the rest later
+          int slot = 0;
+          if (lane == 0) slot = atomicAdd(&S.nrev, 1);
+          slot = __shfl_sync(FULL, slot, 0);
+          if (slot < REV_CAP) {
+            if (lane == 0) {
+              s_rev_u[slot] = u;
+              s_rev_k[slot] = last_key;
+            }
+            break;
+          }
+        }
+        const float* rows[R];
+        float2 st[R];
+        bool on[R];
+        int oidx[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          if (!on[r]) continue;
-          ++n_ref;
-          if (ab[r]) {
-            ++n_ab;
-            continue;
+          unsigned long long best = ~0ull;
+#pragma unroll
+          for (int i = 0; i < WMAX; ++i)
+            if (lbv[i] <= thr) {
+              const unsigned long long key = pack(lbv[i], (uint32_t)(i * 32 + lane));
+              best = key < best ? key : best;
+            }
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) {
+            const unsigned long long other = __shfl_xor_sync(FULL, best, o);
+            best = other < best ? other : best;
           }
-          bool ins;
-          if (S.gslot >= 0) {
-            ins = d2[r] <= *(volatile float*)&S.bsf;
-          } else {
-            const int n = *(volatile int*)&S.tkn;
-            const float kd = *(volatile float*)&s_tkd[n > 0 ? n - 1 : 0];
-            ins = n < A.k || d2[r] <= kd;
+          on[r] = best != ~0ull;
+          oidx[r] = -1;
+          rows[r] = A.series;
+          st[r] = make_float2(0.f, 0.f);
+          if (on[r]) {
+            last_key = best;
+            const int slot = (int)(uint32_t)best;
+#pragma unroll
+            for (int i = 0; i < WMAX; ++i)
+              if (slot == i * 32 + lane) lbv[i] = __int_as_float(0x7fffffff);  // taken
+            const int64_t pos = base + slot;
+            oidx[r] = A.perm[pos];
+            st[r] = A.stats[pos];
+            rows[r] = A.series + (int64_t)oidx[r] * A.len;
           }
-          if (ins) topk_insert(A, S, s_tkd, s_tki, d2[r], oidx[r]);
+        }
+        float d2[R];
+        bool ab[R];
+        ed_warp_multi<NF, R>(rows, st, on, s_qh4, nf4, bsf, d2, ab);
+        if (lane == 0) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (!on[r]) continue;
+            ++n_ref;
+            if (ab[r]) {
+              ++n_ab;
+              continue;
+            }
+            bool ins;
+            if (S.gslot >= 0) {
+              ins = d2[r] <= *(volatile float*)&S.bsf;
+            } else {
+              const int n = *(volatile int*)&S.tkn;
+              const float kd = *(volatile float*)&s_tkd[n > 0 ? n - 1 : 0];
+              ins = n < A.k || d2[r] <= kd;
+            }
+            if (ins) topk_insert(A, S, s_tkd, s_tki, d2[r], oidx[r]);
+          }
         }
       }
     }
+    __syncthreads();
+    if (tid == 0) S.next = 0;
+    __syncthreads();
+    if (S.nrev == 0) break;
   }
   n_cand = __reduce_add_sync(FULL, n_cand);
   n_words = __reduce_add_sync(FULL, n_words);
@@ -1240,6 +1276,8 @@ int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_
   A.lb_rows = lb_rows;
   A.front_batches = 64;
   if (const char* e = getenv("SOFA_FRONT_BATCHES")) A.front_batches = atoi(e) > 0 ? atoi(e) : 1;  // tuning knob
+  A.rev_rounds = 2;
+  if (const char* e = getenv("SOFA_REV_ROUNDS")) A.rev_rounds = atoi(e);  // tuning knob
   A.series = ix->series;
   A.n = ix->n;
   A.nb = ix->nb;
