@@ -243,6 +243,7 @@ def main():
     # ---------------------------------------------------------------- timed steps
     times = []
     launches0 = S.sofa_launch_count()
+    index.kernel_timing(1)  # per-kernel-group CUDA events inside every timed step (no sync)
     with Clocks(local) as clk:
         for s in range(a.steps):
             if not a.no_flush:
@@ -257,6 +258,7 @@ def main():
             barrier()
             times.append(s0.elapsed_time(s1))
         launches = S.sofa_launch_count() - launches0
+        km_tot, km_groups = index.kernel_timing(0)
         # keep sampling clocks for a short sustained run of the same step (no timing taken)
         t_end = time.time() + 1.0
         while time.time() < t_end:
@@ -267,12 +269,13 @@ def main():
     value = w.n_queries * a.steps / (tot_ms / 1e3)
 
     # ---------------------------------------------------------------- roofline of the dominant kernel
-    # Per-kernel GPU times come from the library's CUDA events on the launching stream (sofa_knn
-    # with stats, same launch configuration as the timed steps): front (a5-a8 per query), dense
-    # pass (tcgen05 TF32 screen + exact refine, f1) and scan (a7-a8 task pool).
+    # Per-kernel GPU times: the library's CUDA events on the launching stream, recorded inside every
+    # timed step (sofa_kernel_timing) and averaged over the K steps: front (a5-a8 per query), dense
+    # pass (tcgen05 TF32 screen + exact refine, f1) and scan (a7-a8 task pool).  The work counts
+    # (words, refines, ...) come from the stats call before the timed region (same inputs).
     hbm, peak_kind = peaks()
     bf16 = tensor_peak()
-    km = st["kernel_ms"]
+    km = {kk: v / a.steps for kk, v in km_tot.items()}
     l_b, n_b = w.l, 4 * w.length
     # sparse path (front + scan): algorithmic bytes = envelope nodes (2l B) + words scanned (l B)
     # + rows refined (4n B) + query rows (4n B)  (SURVEY 8(d) unit costs)

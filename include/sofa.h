@@ -236,6 +236,17 @@ const char* sofa_last_error(void);
 /* Process-wide count of kernels this library has launched (bench evidence). */
 int64_t sofa_launch_count(void);
 
+/* Live per-kernel timing of sofa_knn calls without stats (bench.py's roofline, measured over its
+ * timed region).  While enabled, every sofa_knn sub-batch records four CUDA events on the call's
+ * stream (before the front, after it, after the dense pass, after the scan) and nothing else: no
+ * synchronisation, no counters.  Each call to this function first drains the recorded events
+ * (blocking until the last recorded sub-batch has finished), adds their elapsed times to the
+ * totals and, if out_ms / out_groups are non-NULL, writes the totals: out_ms[3] = summed GPU ms of
+ * the front, dense and scan launch groups, *out_groups = sub-batches timed.  Then enable = 1 clears
+ * the totals and starts timing, 0 clears them and stops, -1 leaves the state unchanged (read only).
+ * Errors: SOFA_EINVAL for a NULL index; CUDA errors as SOFA_ECUDA. */
+int sofa_kernel_timing(sofa_index* ix, int32_t enable, double* out_ms, int64_t* out_groups);
+
 #ifdef __cplusplus
 }
 #endif

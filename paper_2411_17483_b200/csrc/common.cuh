@@ -3,8 +3,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <array>
 #include <atomic>
 #include <string>
+#include <vector>
 
 #include "../../include/sofa.h"
 
@@ -264,6 +266,11 @@ struct sofa_index {
   long long* trace = nullptr;  // per-query trace (filled when stats are requested)
   int64_t trace_cap = 0;
   int trace_on = 0;
+  // live per-launch-group timing (sofa_kernel_timing): 4 events per sub-batch, read back lazily
+  int ktime_on = 0;
+  std::vector<std::array<cudaEvent_t, 4>> ktime_pending, ktime_free;
+  double ktime_ms[3] = {0, 0, 0};
+  int64_t ktime_groups = 0;
   int64_t trace_off = 0;  // first query row of the current sub-batch in the trace
   int32_t trace_q = 0;
   // host-path staging

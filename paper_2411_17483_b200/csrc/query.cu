@@ -1274,7 +1274,7 @@ int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_
   A.lb_out = lb_out;
   A.ed_out = ed_out;
   A.lb_rows = lb_rows;
-  A.front_batches = 64;
+  A.front_batches = 16;
   if (const char* e = getenv("SOFA_FRONT_BATCHES")) A.front_batches = atoi(e) > 0 ? atoi(e) : 1;  // tuning knob
   A.rev_rounds = 2;
   if (const char* e = getenv("SOFA_REV_ROUNDS")) A.rev_rounds = atoi(e);  // tuning knob

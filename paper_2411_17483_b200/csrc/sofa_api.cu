@@ -136,6 +136,32 @@ const char* sofa_last_error(void) { return g_err.c_str(); }
 
 int64_t sofa_launch_count(void) { return g_launches.load(); }
 
+int sofa_kernel_timing(sofa_index* ix, int32_t enable, double* out_ms, int64_t* out_groups) {
+  g_err.clear();
+  if (!ix) return fail(SOFA_EINVAL, "index is NULL");
+  // drain what was recorded so far: blocks until the last recorded group has finished
+  if (!ix->ktime_pending.empty()) SOFA_CK(cudaEventSynchronize(ix->ktime_pending.back()[3]));
+  for (auto& quad : ix->ktime_pending) {
+    for (int i = 0; i < 3; ++i) {
+      float ms = 0.f;
+      SOFA_CK(cudaEventElapsedTime(&ms, quad[i], quad[i + 1]));
+      ix->ktime_ms[i] += ms;
+    }
+    ++ix->ktime_groups;
+    ix->ktime_free.push_back(quad);
+  }
+  ix->ktime_pending.clear();
+  if (out_ms)
+    for (int i = 0; i < 3; ++i) out_ms[i] = ix->ktime_ms[i];
+  if (out_groups) *out_groups = ix->ktime_groups;
+  if (enable >= 0) {  // (re)start: clear the totals
+    ix->ktime_on = enable != 0;
+    for (double& m : ix->ktime_ms) m = 0;
+    ix->ktime_groups = 0;
+  }
+  return SOFA_OK;
+}
+
 int sofa_default_opts(sofa_build_opts* out) {
   if (!out) return fail(SOFA_EINVAL, "out is NULL");
   memset(out, 0, sizeof(*out));
@@ -162,6 +188,9 @@ int sofa_learn_model(const float* sample_dev, int64_t S, int32_t len, int32_t l,
 void sofa_free(sofa_index* ix) {
   if (!ix) return;
   free_dense_scratch(ix);
+  for (auto* v : {&ix->ktime_pending, &ix->ktime_free})
+    for (auto& quad : *v)
+      for (auto e : quad) cudaEventDestroy(e);
   void* bufs[] = {ix->qstate, ix->q_T, ix->q_hat, ix->pool, ix->tasks, ix->rank_count, ix->words, ix->stats, ix->stats_orig, ix->perm, ix->env, ix->bkey, ix->basis32, ix->basis64, ix->edges32,
                   ix->edges64, ix->gscratch, ix->qcounter, ix->dstats, ix->hq_dev, ix->hd_dev, ix->hi_dev,
                   ix->trace};
@@ -369,6 +398,18 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
   double kms[3] = {0, 0, 0};
   rc = SOFA_OK;
   for (int q0 = 0; q0 < q && !rc; q0 += qb_max) {
+    // live timing (sofa_kernel_timing): the same four points, recorded without synchronising
+    if (!stats && ix->ktime_on) {
+      if (ix->ktime_free.empty()) {
+        std::array<cudaEvent_t, 4> quad{};
+        for (auto& e : quad) SOFA_CK(cudaEventCreate(&e));
+        ix->ktime_free.push_back(quad);
+      }
+      ix->ktime_pending.push_back(ix->ktime_free.back());
+      ix->ktime_free.pop_back();
+      for (int i = 0; i < 4; ++i) ev[i] = ix->ktime_pending.back()[i];
+    }
+    const bool rec = stats || ix->ktime_on;
     const int qb = q - q0 < qb_max ? q - q0 : qb_max;
     const float* Qb = queries_dev + (int64_t)q0 * ix->len;
     const float* Bb = bsf_init_dev ? bsf_init_dev + q0 : nullptr;
@@ -376,10 +417,10 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
     int64_t* Ib = out_idx_dev + (int64_t)q0 * k;
     ix->trace_off = q0;
     if (dense) SOFA_CK(cudaMemsetAsync(ix->dense.counters, 0, 64 + 1024 * 4, st));
-    if (stats) cudaEventRecord(ev[0], st);
+    if (rec) cudaEventRecord(ev[0], st);
     if (ix->n == 0) {
       rc = launch_fill_pad(Db, Ib, (int64_t)qb * k, st);
-      if (stats) {
+      if (rec) {
         cudaEventRecord(ev[1], st);
         cudaEventRecord(ev[2], st);
       }
@@ -388,13 +429,13 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
       // (every other leaf chunk of every query, spread over all CTAs); the dense and scan kernels read
       // the batch decision from device counters, so there is no host synchronisation in between
       rc = launch_query(ix, Qb, qb, k, Bb, Db, Ib, st, false);
-      if (stats) cudaEventRecord(ev[1], st);
+      if (rec) cudaEventRecord(ev[1], st);
       if (!rc && dense) rc = launch_dense(ix, qb, k, Db, Ib, stats != nullptr, st);
-      if (stats) cudaEventRecord(ev[2], st);
+      if (rec) cudaEventRecord(ev[2], st);
       if (!rc) rc = launch_query(ix, Qb, qb, k, Bb, Db, Ib, st, true);
     }
+    if (rec) cudaEventRecord(ev[3], st);
     if (stats) {
-      cudaEventRecord(ev[3], st);
       cudaEventSynchronize(ev[3]);
       for (int i = 0; i < 3; ++i) {
         float ms = 0.f;

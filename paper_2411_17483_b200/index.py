@@ -78,6 +78,12 @@ class SofaIndex:
         S.sofa_lower_bounds(self.handle, queries.contiguous(), q, m, lb2, ed2, rows, stream)
         return lb2, ed2, rows
 
+    def kernel_timing(self, enable: int = -1) -> tuple[dict, int]:
+        """Live per-launch-group GPU times of knn calls: returns the totals recorded since the last
+        (re)start ({front, dense, scan} ms, sub-batches), then starts (1), stops (0) or keeps (-1)
+        timing.  CUDA events only, no synchronisation inside knn (include/sofa.h)."""
+        return S.sofa_kernel_timing(self.handle, enable)
+
     # -------------------------------------------------------------------------------- introspection
     @property
     def model(self) -> dict:

@@ -89,6 +89,7 @@ def lib() -> C.CDLL:
         L = C.CDLL(LIB)
         L.sofa_last_error.restype = C.c_char_p
         L.sofa_launch_count.restype = I64
+        L.sofa_kernel_timing.argtypes = [VP, I32, VP, P(I64)]
         L.sofa_default_opts.argtypes = [P(sofa_build_opts)]
         L.sofa_learn_model.argtypes = [VP, I64, I32, I32, I32, P(sofa_build_opts), VP, P(sofa_model)]
         L.sofa_build.argtypes = [VP, I64, I32, I32, I32, P(sofa_build_opts), VP, P(VP)]
@@ -134,6 +135,15 @@ def sofa_last_error() -> str:
 
 def sofa_launch_count() -> int:
     return int(lib().sofa_launch_count())
+
+
+def sofa_kernel_timing(ix: int, enable: int) -> tuple[dict, int]:
+    """drain the live timing events; returns ({front, dense, scan} summed ms, sub-batches timed) and
+    then enables (1), disables (0) or keeps (-1) timing; see include/sofa.h"""
+    ms = (C.c_double * 3)()
+    groups = I64(0)
+    _ck(lib().sofa_kernel_timing(ix, enable, ms, C.byref(groups)))
+    return dict(zip(("front", "dense", "scan"), map(float, ms))), int(groups.value)
 
 
 def sofa_default_opts() -> sofa_build_opts:

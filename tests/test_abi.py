@@ -106,3 +106,4 @@ def test_knn_and_merge_reject_bad_args(L):
         sofa.sofa_merge_topk(None, None, 0, 1, 1, None, None, stream=0)
     m = sofa.sofa_model()
     assert L.sofa_transform(None, 5, ctypes.byref(m), None, None, None) == -1
+    assert L.sofa_kernel_timing(None, 1, None, None) == -1 and "NULL" in sofa.sofa_last_error()

@@ -304,6 +304,16 @@ def test_large_batch_runs_in_sub_batches():
     assert_knn_parity(d[pick].cpu().numpy(), i[pick].cpu().numpy(), do, io, x.cpu().numpy(), q[pick].cpu().numpy())
     d1, i1 = ix.knn(q[1000:1100].contiguous(), 3)  # a batch straddling the split gives the same rows
     assert torch.equal(i1, i[1000:1100]) and torch.equal(d1, d[1000:1100])
+    # live kernel timing (bench.py's roofline): one event group per sub-batch, results unchanged
+    ix.kernel_timing(1)
+    d2, i2 = ix.knn(q, 3)
+    d3, i3 = ix.knn(q[:10].contiguous(), 3)
+    km, groups = ix.kernel_timing(0)
+    assert groups == 3 + 1 and km["front"] > 0 and km["scan"] > 0 and km["dense"] >= 0
+    assert torch.equal(i2, i) and torch.equal(d2, d) and torch.equal(i3, i[:10])
+    assert ix.kernel_timing(-1) == ({"front": 0.0, "dense": 0.0, "scan": 0.0}, 0)  # stopped and cleared
+    ix.knn(q[:10].contiguous(), 3)
+    assert ix.kernel_timing(-1)[1] == 0
 
 
 def test_max_k_and_single_query():
