@@ -186,11 +186,12 @@ int sofa_knn_host(sofa_index* ix, const float* queries_host, int32_t q, int32_t 
 int sofa_merge_topk(const float* dist_dev, const int64_t* idx_dev, int32_t parts, int32_t q, int32_t k,
                     float* out_dist_dev, int64_t* out_idx_dev, void* cuda_stream);
 
-/* Per-query trace of the last sofa_knn call made WITH `stats` on this index: q rows of 20 int64
+/* Per-query trace of the last sofa_knn call made WITH `stats` on this index: q rows of 24 int64
  * (SM cycles of prep+tables, seed, tree, scan+refine; blocks_survived, words_scanned, candidates,
  * refined, abandoned, env_nodes, list_blocks, rounds, batches, waves; CTA id; SM id; dense-path
- * decision inputs: flagged, leaves after the take round, take-word passes, take words), copied to
- * out_host (q x 20).  Errors: EINVAL if no such trace. */
+ * decision inputs: flagged, leaves after the take round, take-word passes, take words; the
+ * scan+refine cycles split into top-M seeding, dense decision, the front's leaf scans and the rest
+ * (sorts, filters, task publishing)), copied to out_host (q x 24).  Errors: EINVAL if no such trace. */
 int sofa_knn_trace(const sofa_index* ix, int64_t* out_host, int32_t q);
 
 /* Lower-bound evaluation (TLB): for each of q queries and m index rows at

@@ -10,7 +10,7 @@
 
 #include "../../include/sofa.h"
 
-#define SOFA_TRACE_FIELDS 20
+#define SOFA_TRACE_FIELDS 24
 
 namespace sofa {
 

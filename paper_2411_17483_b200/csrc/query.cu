@@ -696,14 +696,19 @@ __device__ void seed_topm(const QArgs& A, QShared& S, const unsigned long long* 
   for (int u = warp; u < cnt * ppl; u += NW) {
     const unsigned long long ent = list[u / ppl];
     const int64_t base = (int64_t)(uint32_t)ent * B + (int64_t)(u % ppl) * span;
+    uint4 wr[WMAX][NC];  // all loads of the unit in flight together
+#pragma unroll
+    for (int i = 0; i < WMAX; ++i) {
+      const int64_t pos = base + i * 32 + lane;
+      const bool ok = i < wpl && pos < A.n;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) wr[i][c] = ok ? ld_stream_u4(A.words + pos * A.WS + 16 * c) : make_uint4(0u, 0u, 0u, 0u);
+    }
 #pragma unroll
     for (int i = 0; i < WMAX; ++i) {
       const int64_t pos = base + i * 32 + lane;
       if (i < wpl && pos < A.n) {
-        uint4 wr[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) wr[c] = ld_stream_u4(A.words + pos * A.WS + 16 * c);
-        const float lb = word_lb<LT>(reinterpret_cast<const uint4(&)[NC]>(wr), s_T, thr);
+        const float lb = word_lb<LT>(wr[i], s_T, thr);
         ++n_words;
         unsigned long long key = lb <= thr ? pack(lb, (uint32_t)pos) : ~0ull;
 #pragma unroll
@@ -805,7 +810,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
     __syncthreads();
     const int qi = S.qi;
     if (qi >= A.q) break;
-    long long t_phase[5];
+    long long t_phase[5], t_sub[2] = {0, 0}, t_blocks = 0;
     t_phase[0] = clock64();
     // ---------------------------------------------------------------- a5: z-norm + projection
     if (warp == 0) {
@@ -990,6 +995,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
         gl = gl2;
         gl2 = t;
       }
+      t_sub[0] = clock64();  // top-M seeding done
       if (A.mode == 3) {  // sofa_knn_seed: this shard's bound on the k-th best, nothing else
         if (tid == 0) A.seed_out[qi] = S.tkn == A.k ? S.bsf : INFINITY;
         __syncthreads();
@@ -1086,6 +1092,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
           }
         }
       }
+      t_sub[1] = clock64();  // dense decision done
       // the remaining leaves, in ascending LB (MESSI's priority-queue order): up to
       // `budget` of them are scanned here with the stop rule; what a heavy query has left beyond that
       // becomes scan tasks spread over all CTAs.  A dense candidate's leaves are only published
@@ -1105,7 +1112,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
         bitonic_sort_u64(s_blist, cnt);
         int nloc = dc ? 0 : (cnt < budget ? cnt : budget);
         if (!dc && cnt - nloc <= CH) nloc = cnt;  // short remainder: finish it here
-        if (nloc) scan_blocks<LT, NF>(A, S, s_blist, nloc, true, s_T, s_tkd, s_tki, s_qh4);
+        if (nloc) {
+          const long long c0 = clock64();
+          scan_blocks<LT, NF>(A, S, s_blist, nloc, true, s_T, s_tkd, s_tki, s_qh4);
+          t_blocks += clock64() - c0;
+        }
         int rest = cnt - nloc;
         if (!dc && rest > 0 && lb_of(s_blist[nloc]) > S.thr) rest = 0;  // stop rule: nothing left below the BSF
         publish_tasks<LT>(A, S, qi, s_blist + nloc, rest, true, dc);
@@ -1127,7 +1138,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
         const int nrem = S.rem;
         bitonic_sort_u64(s_blist, ntake);
         const int nloc = dc ? 0 : (ntake < budget ? ntake : budget);
-        if (nloc) scan_blocks<LT, NF>(A, S, s_blist, nloc, true, s_T, s_tkd, s_tki, s_qh4);
+        if (nloc) {
+          const long long c0 = clock64();
+          scan_blocks<LT, NF>(A, S, s_blist, nloc, true, s_T, s_tkd, s_tki, s_qh4);
+          t_blocks += clock64() - c0;
+        }
         int rest = ntake - nloc;
         if (!dc && rest > 0 && lb_of(s_blist[nloc]) > S.thr) rest = 0;
         publish_tasks<LT>(A, S, qi, s_blist + nloc, rest, true, dc);
@@ -1184,6 +1199,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
     if (tid == 0 && A.trace) {
       long long* tr = A.trace + (int64_t)qi * SOFA_TRACE_FIELDS;
       for (int i = 0; i < 4; ++i) tr[i] = t_phase[i + 1] - t_phase[i];
+      // the scan phase split: top-M seeding, dense decision, front scan_blocks, the rest (sorts,
+      // filters, task publishing)
+      if (t_sub[0] && t_sub[1]) {
+        tr[20] = t_sub[0] - t_phase[3];
+        tr[21] = t_sub[1] - t_sub[0];
+        tr[22] = t_blocks;
+        tr[23] = t_phase[4] - t_sub[1] - t_blocks;
+      } else {
+        tr[20] = tr[21] = tr[22] = tr[23] = 0;
+      }
       for (int i = 0; i < 10; ++i) tr[4 + i] = S.st[i];
       tr[14] = blockIdx.x;
       for (int i = 0; i < 4; ++i) tr[16 + i] = s_dec[i];

@@ -183,7 +183,8 @@ def sofa_merge_topk(dist_dev, idx_dev, parts, q, k, out_dist_dev, out_idx_dev, s
 
 TRACE_FIELDS = ("cyc_prep", "cyc_seed", "cyc_tree", "cyc_scan", "blocks_survived", "words_scanned",
                 "candidates", "refined", "abandoned", "env_nodes", "list_blocks", "rounds", "batches", "waves",
-                "cta", "sm", "dense_flag", "leaves_after_take", "take_pass", "take_words")
+                "cta", "sm", "dense_flag", "leaves_after_take", "take_pass", "take_words",
+                "cyc_scan_topm", "cyc_scan_decide", "cyc_scan_blocks", "cyc_scan_rest")
 
 
 def sofa_knn_trace(ix, q) -> np.ndarray:

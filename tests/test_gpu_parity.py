@@ -341,3 +341,26 @@ def test_knn_seed_bound_is_a_valid_upper_bound(kind, k):
     d1, i1 = ix.knn(q, k)
     d2, i2 = ix.knn(q, k, bsf_init=torch.from_numpy(b.astype(np.float32)).cuda())
     assert torch.equal(i1, i2) and torch.equal(d1, d2)
+
+
+@pytest.mark.parametrize("rev_rounds", ["0", "1", "1000000"])
+@pytest.mark.parametrize("kind,k,front_batches", [("cfg1", 5, "16"), ("cfg4", 3, "2")])
+def test_revisit_pass_and_front_split(monkeypatch, rev_rounds, kind, k, front_batches):
+    """scan_blocks' revisit pass (a leaf part with more than rev_rounds x R candidates is deferred
+    until after the list; 0 defers every part with a candidate and overflows the revisit queue,
+    1e6 never defers) and the front/scan split (front_batches word batches in the front, the rest
+    as scan tasks) change the refinement order only: results equal the oracle's brute force and
+    each other bit for bit (tuning knobs read by the library at every launch)"""
+    monkeypatch.setenv("SOFA_REV_ROUNDS", rev_rounds)
+    monkeypatch.setenv("SOFA_FRONT_BATCHES", front_batches)
+    w = datagen.scaled(datagen.WORKLOADS[kind], 200_000 + 33, 24)
+    x, q = _data(w)
+    ix = SofaIndex(x, sample_size=3000, dense_permille=-1)
+    d, i, st = ix.knn(q, k, stats=True)
+    torch.cuda.synchronize()
+    do, io = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), k)
+    assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, x.cpu().numpy(), q.cpu().numpy())
+    monkeypatch.setenv("SOFA_REV_ROUNDS", "1000000")
+    monkeypatch.setenv("SOFA_FRONT_BATCHES", "1000000")
+    d2, i2 = ix.knn(q, k)
+    assert torch.equal(d, d2) and torch.equal(i, i2)
