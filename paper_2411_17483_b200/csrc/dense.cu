@@ -321,11 +321,13 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       }
       const int acc = (int)(local & 1);
       const uint32_t aph = (uint32_t)((local >> 1) & 1);
-      float2* ser = s_ser2 + acc * DN;     // (-2 inv, |x^|^2), +inf |x^|^2 past the last row
+      float2* ser = s_ser2 + acc * DN;     // (-2 inv, |x^|^2), NaN |x^|^2 past the last row
       float* tmx = s_tmax + acc * 4;      // tile maxima: inv |x|, slack_s, |2 mu inv|
       {
         const int64_t s = t * DN + et;
-        float2 v = make_float2(0.f, INFINITY);
+        // past the last row: NaN, never <= any threshold (+inf would pass an infinite one, i.e.
+        // while a query holds fewer than k results)
+        float2 v = make_float2(0.f, __int_as_float(0x7fffffff));
         float e = 0.f, rs = 0.f, b = 0.f;
         if (s < A.n) {
           const float2 st = A.stats_orig[s];

@@ -264,7 +264,7 @@ __device__ void topk_insert(const QArgs& A, QShared& S, float* s_tkd, int* s_tki
 // warp's improvement prunes the other warps' candidates at once; no CTA barrier inside the loop.
 template <int LT, int NF>
 __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long* list, int cnt, bool sorted,
-                            const float* s_T, float* s_tkd, int* s_tki, const float4* s_qh4) {
+                            const float* s_T, float* s_tkd, int* s_tki, const float4* s_qh4, int seed_rounds = 0) {
   constexpr int NC = LT / 16;
   constexpr int WMAX = 8 / NC;                          // words per lane per unit
   constexpr int R = NF <= 2 ? 4 : (NF <= 4 ? 2 : 1);  // rows refined together per warp
@@ -349,6 +349,7 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
 #pragma unroll
         for (int i = 0; i < WMAX; ++i) mine |= lbv[i] <= thr;
         if (!__any_sync(FULL, mine)) break;  // the common case: no candidate left in this unit
+        if (seed_rounds > 0 && rounds == seed_rounds) break;  // seed leaf: it is scanned again from the list
         if (pass == 0 && rounds == A.rev_rounds) {  // many candidates: a loose BSF; revisit the rest later
           int slot = 0;
           if (lane == 0) slot = atomicAdd(&S.nrev, 1);
@@ -858,19 +859,38 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
     for (int j = warp; j < LT; j += 8) {
       double acc = 0.0;
       if (j < l)
-        for (int t = lane; t < len; t += 32) acc = fma(s_qd[t], A.basis64[(int64_t)j * len + t], acc);
+        for (int t0 = lane; t0 < len; t0 += 32 * 8) {  // 8 loads in flight, same summation order
+          double b[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) b[u] = t0 + 32 * u < len ? A.basis64[(int64_t)j * len + t0 + 32 * u] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (t0 + 32 * u < len) acc = fma(s_qd[t0 + 32 * u], b[u], acc);
+        }
       acc = warp_sum_f64(acc);
       if (lane == 0) s_qproj[j] = acc;
     }
     __syncthreads();
     // ---------------------------------------------------------------- a5: LB tables (round down)
-    for (int e = tid; e < LT * 256; e += kThreads) {
+    for (int e0 = tid; e0 < LT * 256; e0 += kThreads * 4) {
+      double elo[4], ehi[4];  // the bin edges of 4 entries, loads in flight together
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * kThreads, j = e >> 8, s = e & 255;
+        const bool v = e < LT * 256 && j < l && s < a;
+        elo[u] = !v || s == 0 ? -INFINITY : A.edges64[j * 256 + s - 1];
+        ehi[u] = !v || s == a - 1 ? INFINITY : A.edges64[j * 256 + s];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * kThreads;
+      if (e >= LT * 256) break;
       const int j = e >> 8, s = e & 255;
       float t = 0.f, tlo = 0.f, thi = 0.f;
       if (j < l && s < a) {
         const double qv = s_qproj[j], w = (double)A.weights[j];
-        const double lo = s == 0 ? -INFINITY : A.edges64[j * 256 + s - 1];
-        const double hi = s == a - 1 ? INFINITY : A.edges64[j * 256 + s];
+        const double lo = elo[u];
+        const double hi = ehi[u];
         const double dl = fmax(0.0, lo - qv), dh = fmax(0.0, qv - hi);
         tlo = __double2float_rd(w * dl * dl);
         thi = __double2float_rd(w * dh * dh);
@@ -881,6 +901,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
       s_T[e] = t;
       s_Tlo[e] = tlo;
       s_Thi[e] = thi;
+      }
     }
     __syncthreads();
     if (A.mode == 2) {
@@ -925,7 +946,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
     t_phase[1] = clock64();
     if (tid == 0) s_seed = pack(0.f, (uint32_t)b0);
     __syncthreads();
-    scan_blocks<LT, NF>(A, S, &s_seed, A.nb > 0 ? 1 : 0, true, s_T, s_tkd, s_tki, s_qh4);
+    // own-key seed: the R lowest-LB words of each warp's part of the leaf, as many rounds as it
+    // takes to fill k; no revisit (the leaf is not excluded from the tree descent below: b0 = -1,
+    // so its remaining candidates are scanned again from the list)
+    scan_blocks<LT, NF>(A, S, &s_seed, A.nb > 0 ? 1 : 0, true, s_T, s_tkd, s_tki, s_qh4,
+                        1 + (A.k - 1) / (kThreads / 32 * (NF <= 2 ? 4 : (NF <= 4 ? 2 : 1))));
     t_phase[2] = clock64();
     // ---------------------------------------------------------------- a6: envelope tree descent
     // top level: every node; lower levels: the kFan children of each surviving parent
@@ -934,13 +959,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
       const float thr = S.thr;
       unsigned long long* cur = gl;
       unsigned long long* nxt = gl2;
-      env_level<LT>(A, A.nlev - 1, nullptr, 0, b0, thr, s_Tlo, s_Thi, cur, &S.cnt, S.st[5]);
+      env_level<LT>(A, A.nlev - 1, nullptr, 0, -1, thr, s_Tlo, s_Thi, cur, &S.cnt, S.st[5]);
       for (int L = A.nlev - 2; L >= 0; --L) {
         __syncthreads();
         const int np = S.cnt;
         if (tid == 0) S.rem = 0;
         __syncthreads();
-        env_level<LT>(A, L, cur, np, b0, S.thr, s_Tlo, s_Thi, nxt, &S.rem, S.st[5]);
+        env_level<LT>(A, L, cur, np, -1, S.thr, s_Tlo, s_Thi, nxt, &S.rem, S.st[5]);
         __syncthreads();
         if (tid == 0) S.cnt = S.rem;
         unsigned long long* t = cur;

@@ -76,6 +76,21 @@ def test_dense_edge_rows_and_bsf_init():
     assert bool((i2[d0 > 0] == -1).all())
 
 
+@pytest.mark.parametrize("N,k", [(37, 37), (37, 20), (300, 128), (513, 100)])
+def test_dense_ragged_tile_with_unfilled_topk(N, k):
+    """the dense screen's last row tile extends past N; while a query holds fewer than k results its
+    threshold is +inf, and the rows past the end must still never become candidates (regression:
+    they carried |x^|^2 = +inf, and +inf <= +inf emitted them)"""
+    rng = np.random.default_rng(N + k)
+    base = np.cumsum(rng.normal(size=(N, 32)), axis=1).astype(np.float32)
+    x = torch.from_numpy(base).cuda()
+    q = torch.from_numpy(base[[0, N // 2, N - 1]] + rng.normal(scale=0.1, size=(3, 32)).astype(np.float32)).cuda()
+    ix, d, i, st = _check(x, q, k, l=4, alphabet=4, sample_size=N, block_size=32, dense_permille=1000)
+    assert st["dense_queries"] == 3
+    assert bool((i >= 0).all()) and bool((i < N).all())
+    assert st["dense_candidates"] <= 3 * N
+
+
 def test_dense_candidate_overflow_falls_back_exactly():
     """a 64-entry candidate buffer overflows; the per-query brute-force fallback keeps results exact"""
     code = r"""
