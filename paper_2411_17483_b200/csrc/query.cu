@@ -255,6 +255,11 @@ __device__ void topk_insert(const QArgs& A, QShared& S, float* s_tkd, int* s_tki
   atomicExch(&S.lock, 0);
 }
 
+// rows a warp refines together in scan_blocks (R): more rows give more loads in flight, but R = 4 at
+// n <= 256 spills at the 80-register cap of 3 CTAs per SM (configs[1] 9% slower than R = 2)
+template <int NF>
+__host__ __device__ constexpr int refine_rows() { return NF <= 4 ? 2 : 1; }
+
 // a7 + a8 over a list of leaves, barrier-free and warp-centric.  Each warp pulls the next unit (a
 // leaf, or a part of one) from a shared counter — in ascending leaf LB when the list is sorted, and
 // stopping at the first leaf whose LB exceeds the BSF (MESSI's priority order and stop rule,
@@ -268,7 +273,7 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
                             const float* s_T, float* s_tkd, int* s_tki, const float4* s_qh4, int seed_rounds = 0) {
   constexpr int NC = LT / 16;
   constexpr int WMAX = 8 / NC;                          // words per lane per unit
-  constexpr int R = NF <= 2 ? 4 : (NF <= 4 ? 2 : 1);  // rows refined together per warp
+  constexpr int R = refine_rows<NF>();  // rows refined together per warp
   constexpr int NW = kThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31;
   if (cnt <= 0) return;
@@ -951,7 +956,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
     // takes to fill k; no revisit (the leaf is not excluded from the tree descent below: b0 = -1,
     // so its remaining candidates are scanned again from the list)
     scan_blocks<LT, NF>(A, S, &s_seed, A.nb > 0 ? 1 : 0, true, s_T, s_tkd, s_tki, s_qh4,
-                        1 + (A.k - 1) / (kThreads / 32 * (NF <= 2 ? 4 : (NF <= 4 ? 2 : 1))));
+                        1 + (A.k - 1) / (kThreads / 32 * refine_rows<NF>()));
     t_phase[2] = clock64();
     // ---------------------------------------------------------------- a6: envelope tree descent
     // top level: every node; lower levels: the kFan children of each surviving parent
