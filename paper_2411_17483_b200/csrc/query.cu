@@ -268,12 +268,12 @@ __host__ __device__ constexpr int refine_rows() { return NF <= 4 ? 2 : 1; }
 // LB: R at a time (the R smallest by warp-min extraction), exact squared ED with early abandoning
 // (P:382), improvements into the shared top-k.  The BSF every warp reads is the shared one, so a
 // warp's improvement prunes the other warps' candidates at once; no CTA barrier inside the loop.
-template <int LT, int NF>
+template <int LT, int NF, int RR = refine_rows<NF>()>
 __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long* list, int cnt, bool sorted,
                             const float* s_T, float* s_tkd, int* s_tki, const float4* s_qh4, int seed_rounds = 0) {
   constexpr int NC = LT / 16;
   constexpr int WMAX = 8 / NC;                          // words per lane per unit
-  constexpr int R = refine_rows<NF>();  // rows refined together per warp
+  constexpr int R = RR;  // rows refined together per warp
   constexpr int NW = kThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31;
   if (cnt <= 0) return;
@@ -490,7 +490,7 @@ __device__ void publish_tasks(const QArgs& A, QShared& S, int q, const unsigned 
 
 // scan mode: all CTAs pull tasks until the pool is drained; rank-major order (every query's lowest-
 // LB chunk first), so a query's later chunks usually meet its final BSF and are rejected unread
-template <int LT, int NF>
+template <int LT, int NF, int RR = refine_rows<NF>()>
 __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd, int* s_tki, float4* s_qh4) {
   const int tid = threadIdx.x;
   bool dense_go = false;
@@ -554,7 +554,7 @@ __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd,
         S.lock = 0;
       }
       __syncthreads();
-      scan_blocks<LT, NF>(A, S, A.pool + tk.off, tk.cnt_flags & kTaskCnt, (tk.cnt_flags & kTaskSorted) != 0, s_T,
+      scan_blocks<LT, NF, RR>(A, S, A.pool + tk.off, tk.cnt_flags & kTaskCnt, (tk.cnt_flags & kTaskSorted) != 0, s_T,
                           s_tkd, s_tki, s_qh4);
       __syncthreads();
     }
@@ -781,7 +781,7 @@ __device__ void seed_topm(const QArgs& A, QShared& S, const unsigned long long* 
   __syncthreads();
 }
 
-template <int LT, int NF>
+template <int LT, int NF, int RR = refine_rows<NF>()>
 __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ QArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ QShared S;
@@ -809,7 +809,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
   unsigned long long* gl2 = gl + A.nb;
 
   if (A.mode == 1) {
-    scan_tasks<LT, NF>(A, S, s_T, s_tkd, s_tki, s_qh4);
+    scan_tasks<LT, NF, RR>(A, S, s_T, s_tkd, s_tki, s_qh4);
     return;
   }
   for (;;) {
@@ -955,8 +955,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
     // own-key seed: the R lowest-LB words of each warp's part of the leaf, as many rounds as it
     // takes to fill k; no revisit (the leaf is not excluded from the tree descent below: b0 = -1,
     // so its remaining candidates are scanned again from the list)
-    scan_blocks<LT, NF>(A, S, &s_seed, A.nb > 0 ? 1 : 0, true, s_T, s_tkd, s_tki, s_qh4,
-                        1 + (A.k - 1) / (kThreads / 32 * refine_rows<NF>()));
+    scan_blocks<LT, NF, RR>(A, S, &s_seed, A.nb > 0 ? 1 : 0, true, s_T, s_tkd, s_tki, s_qh4,
+                            1 + (A.k - 1) / (kThreads / 32 * RR));
     t_phase[2] = clock64();
     // ---------------------------------------------------------------- a6: envelope tree descent
     // top level: every node; lower levels: the kFan children of each surviving parent
@@ -1145,7 +1145,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
         if (!dc && cnt - nloc <= CH) nloc = cnt;  // short remainder: finish it here
         if (nloc) {
           const long long c0 = clock64();
-          scan_blocks<LT, NF>(A, S, s_blist, nloc, true, s_T, s_tkd, s_tki, s_qh4);
+          scan_blocks<LT, NF, RR>(A, S, s_blist, nloc, true, s_T, s_tkd, s_tki, s_qh4);
           t_blocks += clock64() - c0;
         }
         int rest = cnt - nloc;
@@ -1171,7 +1171,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
         const int nloc = dc ? 0 : (ntake < budget ? ntake : budget);
         if (nloc) {
           const long long c0 = clock64();
-          scan_blocks<LT, NF>(A, S, s_blist, nloc, true, s_T, s_tkd, s_tki, s_qh4);
+          scan_blocks<LT, NF, RR>(A, S, s_blist, nloc, true, s_T, s_tkd, s_tki, s_qh4);
           t_blocks += clock64() - c0;
         }
         int rest = ntake - nloc;
@@ -1251,13 +1251,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
   }
 }
 
-template <int LT, int NF>
+template <int LT, int NF, int RR = refine_rows<NF>()>
 static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
   QArgs A = A0;
   constexpr int UB0 = 2 * LT * 256 * 4, UB1 = CAP_B * 8, UB2 = NF * 128 * 8;
   constexpr int UB = UB0 > UB1 ? (UB0 > UB2 ? UB0 : UB2) : (UB1 > UB2 ? UB1 : UB2);
   const size_t smem = NF * 128 * 4 + LT * 8 + LT * 256 * 4 + UB + kThreads * 8 + KMAX * 8;
-  auto kern = k_query<LT, NF>;
+  auto kern = k_query<LT, NF, RR>;
   // launch shape, once per instantiation and device (no driver queries on the per-call path)
   static int cached_dev = -1, per_sm = 0, sms = 148;
   if (cached_dev != ix->device) {
@@ -1392,8 +1392,19 @@ int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_
   for (int j = 0; j < SOFA_MAX_L; ++j) A.weights[j] = j < ix->l ? (float)ix->model.weights[j] : 0.f;
   const int nf4 = ix->len / 4;
   const int NF = nf4 <= 32 ? 1 : nf4 <= 64 ? 2 : nf4 <= 128 ? 4 : 8;
+  // rows per refine round in the front: 2 (no register spills: best when every CTA runs several
+  // queries, configs[1] 0.57 vs 0.62 ms) or, for n <= 256 and at most one query per CTA, 4 (more row
+  // loads in flight per warp: a batch that small is set by its slowest, refine-bound query;
+  // configs[0] 0.55 vs 0.63 ms).  The scan pool is indifferent (measured) and uses 2.
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+  int rsel = A.mode == 0 && A.q <= 3 * sms ? 4 : 2;
+  if (const char* e = getenv(A.mode == 1 ? "SOFA_R_SCAN" : "SOFA_R_FRONT")) rsel = atoi(e);  // tuning knobs
 #define SOFA_Q(lt, nf) \
-  if (ix->LT == lt && NF == nf) return launch_query_t<lt, nf>(ix, A, st);
+  if (ix->LT == lt && NF == nf) {                                                       \
+    if (nf <= 2 && rsel == 4) return launch_query_t<lt, (nf <= 2 ? nf : 1), 4>(ix, A, st); \
+    return launch_query_t<lt, nf>(ix, A, st);                                           \
+  }
   SOFA_Q(16, 1) SOFA_Q(16, 2) SOFA_Q(16, 4) SOFA_Q(16, 8)
   SOFA_Q(32, 1) SOFA_Q(32, 2) SOFA_Q(32, 4) SOFA_Q(32, 8)
   SOFA_Q(64, 1) SOFA_Q(64, 2) SOFA_Q(64, 4) SOFA_Q(64, 8)
