@@ -28,8 +28,19 @@
 
 #include "common.cuh"
 
-namespace sofa {
+// This file is compiled twice: as itself (8-warp CTAs, 3 per SM: batches with several queries per
+// CTA) and through query512.cu (16-warp CTAs, one per SM: batches of at most one query per SM,
+// where a query's latency sets the step).  Each copy lives in its own namespace.
+#ifndef SOFA_QTHREADS
+#define SOFA_QTHREADS 256
+#define SOFA_QNS q256
+#define SOFA_QMAIN 1
+#endif
 
+namespace sofa {
+namespace SOFA_QNS {
+
+constexpr int kQThreads = SOFA_QTHREADS;  // threads per k_query CTA
 constexpr int CAP_B = 2048;  // surviving blocks sorted in shared memory
 constexpr int CAP_C = 2048;  // words per scan batch (l <= 16)
 constexpr int TOPM_MIN_LEAVES = 256;  // top-M seeding for queries whose leaf list is longer than this (at least)
@@ -123,11 +134,11 @@ __device__ __forceinline__ float lb_of(unsigned long long e) { return __uint_as_
 __device__ void bitonic_sort_u64(unsigned long long* s, int n) {
   int P2 = 1;
   while (P2 < n) P2 <<= 1;
-  for (int i = n + threadIdx.x; i < P2; i += kThreads) s[i] = ~0ull;
+  for (int i = n + threadIdx.x; i < P2; i += kQThreads) s[i] = ~0ull;
   __syncthreads();
   for (int k = 2; k <= P2; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P2; i += kThreads) {
+      for (int i = threadIdx.x; i < P2; i += kQThreads) {
         const int ixj = i ^ j;
         if (ixj > i) {
           const unsigned long long a = s[i], b = s[ixj];
@@ -274,7 +285,7 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
   constexpr int NC = LT / 16;
   constexpr int WMAX = 8 / NC;                          // words per lane per unit
   constexpr int R = RR;  // rows refined together per warp
-  constexpr int NW = kThreads / 32;
+  constexpr int NW = kQThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31;
   if (cnt <= 0) return;
   const int B = A.B;
@@ -473,11 +484,11 @@ __device__ void publish_tasks(const QArgs& A, QShared& S, int q, const unsigned 
   __syncthreads();
   const int64_t off = S.off;
   const int r0 = S.chunk;
-  for (int i = tid; i < n; i += kThreads) A.pool[off + i] = list[i];
+  for (int i = tid; i < n; i += kQThreads) A.pool[off + i] = list[i];
   const int flags = sorted ? kTaskSorted : 0;
   ScanTask* tasks = A.tasks + (int64_t)set * A.rank_cap * A.q;
   int* rc = A.rank_count + set * A.rank_cap;
-  for (int i = tid; i < nt; i += kThreads) {
+  for (int i = tid; i < nt; i += kQThreads) {
     ScanTask t;
     t.off = off + (int64_t)i * CH;
     t.q = q;
@@ -541,8 +552,8 @@ __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd,
     if (!S.take) {
       if (q != cur) {
         const float4* T4 = reinterpret_cast<const float4*>(A.q_T + (int64_t)q * LT * 256);
-        for (int i = tid; i < LT * 64; i += kThreads) reinterpret_cast<float4*>(s_T)[i] = T4[i];
-        for (int i = tid; i < A.len; i += kThreads) reinterpret_cast<float*>(s_qh4)[i] = A.q_hat[(int64_t)q * A.len + i];
+        for (int i = tid; i < LT * 64; i += kQThreads) reinterpret_cast<float4*>(s_T)[i] = T4[i];
+        for (int i = tid; i < A.len; i += kQThreads) reinterpret_cast<float*>(s_qh4)[i] = A.q_hat[(int64_t)q * A.len + i];
         cur = q;
       }
       if (tid == 0) {
@@ -567,7 +578,7 @@ __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd,
     __syncthreads();
     if (S.take) {  // last task of this query: write its result
       const int n = h->tkn;
-      for (int r = tid; r < A.k; r += kThreads) {
+      for (int r = tid; r < A.k; r += kQThreads) {
         const bool ok = r < n;
         A.od[(int64_t)q * A.k + r] = ok ? sqrtf(h->tkd[r]) : INFINITY;
         A.oi[(int64_t)q * A.k + r] = ok ? A.goff + h->tki[r] : -1;
@@ -610,7 +621,7 @@ __device__ void env_level(const QArgs& A, int L, const unsigned long long* paren
   const uint8_t* base = A.env + A.lvl_off[L] * 2 * WS;
   const int64_t ncnt = A.lvl_cnt[L];
   const int64_t total = parents ? (int64_t)nparents * kFan : ncnt;
-  for (int64_t ii = (int64_t)warp * 32 * U; ii < total; ii += (int64_t)kThreads * U) {
+  for (int64_t ii = (int64_t)warp * 32 * U; ii < total; ii += (int64_t)kQThreads * U) {
     int64_t node[U];
     bool ok[U];
     uint4 mn[U][NC], mx[U][NC];
@@ -650,7 +661,7 @@ __device__ void filter_list(const unsigned long long* src, int cnt, float thr, f
                             int* ntake, unsigned long long* rem, int* nrem, int cap = CAP_B) {
   constexpr int U = 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int ee = warp * 32 * U; ee < cnt; ee += kThreads * U) {
+  for (int ee = warp * 32 * U; ee < cnt; ee += kQThreads * U) {
     unsigned long long ent[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -689,7 +700,7 @@ __device__ void seed_topm(const QArgs& A, QShared& S, const unsigned long long* 
   constexpr int NC = LT / 16;
   constexpr int WMAX = 8 / NC;
   constexpr int M = 4;  // per warp
-  constexpr int NW = kThreads / 32;
+  constexpr int NW = kQThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int B = A.B;
   int ppl = B / (32 * WMAX);
@@ -782,7 +793,7 @@ __device__ void seed_topm(const QArgs& A, QShared& S, const unsigned long long* 
 }
 
 template <int LT, int NF, int RR = refine_rows<NF>()>
-__global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ QArgs A) {
+__global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(const __grid_constant__ QArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ QShared S;
   constexpr int UB0 = 2 * LT * 256 * 4, UB1 = CAP_B * 8, UB2 = NF * 128 * 8;
@@ -796,7 +807,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
   double* s_qd = reinterpret_cast<double*>(s_u);
   unsigned long long* s_blist = reinterpret_cast<unsigned long long*>(s_u);
   unsigned long long* s_samp = reinterpret_cast<unsigned long long*>(s_u + UB);  // strided list sample
-  float* s_tkd = reinterpret_cast<float*>(s_samp + kThreads);
+  float* s_tkd = reinterpret_cast<float*>(s_samp + kQThreads);
   int* s_tki = reinterpret_cast<int*>(s_tkd + KMAX);
   __shared__ uint8_t s_qw[SOFA_MAX_L];
   __shared__ unsigned long long s_seed;
@@ -862,7 +873,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
       }
     }
     __syncthreads();
-    for (int j = warp; j < LT; j += 8) {
+    for (int j = warp; j < LT; j += kQThreads / 32) {
       double acc = 0.0;
       if (j < l)
         for (int t0 = lane; t0 < len; t0 += 32 * 8) {  // 8 loads in flight, same summation order
@@ -878,18 +889,18 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
     }
     __syncthreads();
     // ---------------------------------------------------------------- a5: LB tables (round down)
-    for (int e0 = tid; e0 < LT * 256; e0 += kThreads * 4) {
+    for (int e0 = tid; e0 < LT * 256; e0 += kQThreads * 4) {
       double elo[4], ehi[4];  // the bin edges of 4 entries, loads in flight together
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int e = e0 + u * kThreads, j = e >> 8, s = e & 255;
+        const int e = e0 + u * kQThreads, j = e >> 8, s = e & 255;
         const bool v = e < LT * 256 && j < l && s < a;
         elo[u] = !v || s == 0 ? -INFINITY : A.edges64[j * 256 + s - 1];
         ehi[u] = !v || s == a - 1 ? INFINITY : A.edges64[j * 256 + s];
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-      const int e = e0 + u * kThreads;
+      const int e = e0 + u * kQThreads;
       if (e >= LT * 256) break;
       const int j = e >> 8, s = e & 255;
       float t = 0.f, tlo = 0.f, thi = 0.f;
@@ -913,7 +924,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
     if (A.mode == 2) {
       // lower-bound evaluation (TLB): for rows at sorted positions floor(j n / m), the squared
       // word LB from this query's table (no abandoning) and the exact squared z-ED
-      for (int64_t j = warp; j < A.lb_m; j += kThreads / 32) {
+      for (int64_t j = warp; j < A.lb_m; j += kQThreads / 32) {
         const int64_t pos = j * A.n / A.lb_m;
         const float* rows[1] = {A.series + (int64_t)A.perm[pos] * len};
         const float2 st[1] = {A.stats[pos]};
@@ -937,7 +948,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
     const uint64_t key = word_key(s_qw, l, 31 - __clz(a));
     int64_t lo = 0, hi = A.nb;
     while (hi - lo > 1) {  // 256-way parallel search: largest b with bkey[b] <= key
-      const int64_t step = (hi - lo + kThreads - 1) / kThreads;
+      const int64_t step = (hi - lo + kQThreads - 1) / kQThreads;
       const int64_t idx = lo + (int64_t)tid * step;
       const int c = __syncthreads_count(idx < hi && A.bkey[idx] <= key);
       if (c == 0) {
@@ -956,7 +967,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
     // takes to fill k; no revisit (the leaf is not excluded from the tree descent below: b0 = -1,
     // so its remaining candidates are scanned again from the list)
     scan_blocks<LT, NF, RR>(A, S, &s_seed, A.nb > 0 ? 1 : 0, true, s_T, s_tkd, s_tki, s_qh4,
-                            1 + (A.k - 1) / (kThreads / 32 * RR));
+                            1 + (A.k - 1) / (kQThreads / 32 * RR));
     t_phase[2] = clock64();
     // ---------------------------------------------------------------- a6: envelope tree descent
     // top level: every node; lower levels: the kFan children of each surviving parent
@@ -980,7 +991,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
       }
       if (cur != gl) {  // the rounds below start from gl
         __syncthreads();
-        for (int i = tid; i < S.cnt; i += kThreads) gl[i] = cur[i];
+        for (int i = tid; i < S.cnt; i += kQThreads) gl[i] = cur[i];
       }
       __syncthreads();  // S.cnt and gl are final for every thread
     }
@@ -996,18 +1007,18 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
       int cnt = S.cnt;
       if (tid == 0) S.st[6] += cnt;
       if (A.mode == 3 && cnt > 0 && cnt <= A.topm_min) {  // seed bound of a short list: top-M over all of it
-        for (int i = tid; i < cnt; i += kThreads) s_blist[i] = gl[i];
+        for (int i = tid; i < cnt; i += kQThreads) s_blist[i] = gl[i];
         __syncthreads();
         seed_topm<LT, NF>(A, S, s_blist, cnt, s_T, s_tkd, s_tki, s_qh4);
       }
       if (cnt > A.topm_min) {
         // top-M seeding over the TOPM_LEAVES lowest-LB leaves (threshold from a sorted strided sample)
-        s_samp[tid] = gl[((int64_t)tid * cnt) / kThreads];
+        s_samp[tid] = gl[((int64_t)tid * cnt) / kQThreads];
         if (tid == 0) S.take = 0;
         __syncthreads();
-        bitonic_sort_u64(s_samp, kThreads);
-        int r = (int)(((int64_t)kThreads * A.topm_leaves) / cnt);
-        r = r < 0 ? 0 : (r > kThreads - 1 ? kThreads - 1 : r);
+        bitonic_sort_u64(s_samp, kQThreads);
+        int r = (int)(((int64_t)kQThreads * A.topm_leaves) / cnt);
+        r = r < 0 ? 0 : (r > kQThreads - 1 ? kQThreads - 1 : r);
         const float tau = lb_of(s_samp[r]);
         filter_list(gl, cnt, S.thr, tau, s_blist, &S.take, nullptr, nullptr, A.topm_leaves);
         __syncthreads();
@@ -1042,12 +1053,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
         // the list); if most of them still pass the (nearly final) BSF and many leaves survive, the
         // SFA bound cannot prune this query and it goes to the batched dense path.
         constexpr int TAKE0 = 8;
-        s_samp[tid] = gl[((int64_t)tid * cnt) / kThreads];
+        s_samp[tid] = gl[((int64_t)tid * cnt) / kQThreads];
         if (tid == 0) S.take = 0;
         __syncthreads();
-        bitonic_sort_u64(s_samp, kThreads);
-        int r = (int)(((int64_t)kThreads * TAKE0) / cnt);
-        r = r < 0 ? 0 : (r > kThreads - 1 ? kThreads - 1 : r);
+        bitonic_sort_u64(s_samp, kQThreads);
+        int r = (int)(((int64_t)kQThreads * TAKE0) / cnt);
+        r = r < 0 ? 0 : (r > kQThreads - 1 ? kQThreads - 1 : r);
         const float tau = lb_of(s_samp[r]);
         filter_list(gl, cnt, S.thr, tau, s_blist, &S.take, nullptr, nullptr, TAKE0);
         __syncthreads();
@@ -1062,7 +1073,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
         if (cnt >= A.dense_min) {
           const float thr = S.thr;
           const int nw = ntake * A.B < 2048 ? ntake * A.B : 2048;
-          for (int w = tid; w < nw; w += kThreads) {
+          for (int w = tid; w < nw; w += kQThreads) {
             const int64_t pos = (int64_t)(uint32_t)s_blist[w / A.B] * A.B + (w % A.B);
             if (pos < A.n) {
               uint4 wr[LT / 16];
@@ -1093,8 +1104,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
       if (s_dense >= 0) {
         // publish the query's state to its dense slot; dense.cu finishes it
         const int slot = s_dense;
-        for (int t = tid; t < len; t += kThreads) A.d_qhat[(int64_t)slot * len + t] = reinterpret_cast<const float*>(s_qh4)[t];
-        for (int r = tid; r < S.tkn; r += kThreads) {
+        for (int t = tid; t < len; t += kQThreads) A.d_qhat[(int64_t)slot * len + t] = reinterpret_cast<const float*>(s_qh4)[t];
+        for (int r = tid; r < S.tkn; r += kQThreads) {
           A.d_tkd[(int64_t)slot * A.k + r] = s_tkd[r];
           A.d_tki[(int64_t)slot * A.k + r] = s_tki[r];
         }
@@ -1138,7 +1149,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
         // as they are (one pass; no ordering work for a list that is usually never scanned)
         publish_tasks<LT>(A, S, qi, gl, cnt, false, true);
       } else if (cnt <= CAP_B) {
-        for (int i = tid; i < cnt; i += kThreads) s_blist[i] = gl[i];
+        for (int i = tid; i < cnt; i += kQThreads) s_blist[i] = gl[i];
         __syncthreads();
         bitonic_sort_u64(s_blist, cnt);
         int nloc = dc ? 0 : (cnt < budget ? cnt : budget);
@@ -1153,15 +1164,15 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
         publish_tasks<LT>(A, S, qi, s_blist + nloc, rest, true, dc);
       } else {
         if (tid == 0) S.st[7] += 1;
-        s_samp[tid] = gl[((int64_t)tid * cnt) / kThreads];
+        s_samp[tid] = gl[((int64_t)tid * cnt) / kQThreads];
         if (tid == 0) {
           S.take = 0;
           S.rem = 0;
         }
         __syncthreads();
-        bitonic_sort_u64(s_samp, kThreads);
-        int r = (int)(((int64_t)kThreads * (CAP_B * 3 / 4)) / cnt);
-        r = r < 0 ? 0 : (r > kThreads - 1 ? kThreads - 1 : r);
+        bitonic_sort_u64(s_samp, kQThreads);
+        int r = (int)(((int64_t)kQThreads * (CAP_B * 3 / 4)) / cnt);
+        r = r < 0 ? 0 : (r > kQThreads - 1 ? kQThreads - 1 : r);
         const float tau = lb_of(s_samp[r]);
         filter_list(gl, cnt, S.thr, tau, s_blist, &S.take, gl2, &S.rem);
         __syncthreads();
@@ -1195,9 +1206,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
           atomicAdd(&A.dstats[22], (unsigned long long)S.ntask);
           atomicAdd(&A.dstats[23], 1ull);
         }
-        for (int i = tid; i < LT * 256; i += kThreads) A.q_T[(int64_t)qi * LT * 256 + i] = s_T[i];
-        for (int i = tid; i < len; i += kThreads) A.q_hat[(int64_t)qi * len + i] = reinterpret_cast<const float*>(s_qh4)[i];
-        for (int r = tid; r < S.tkn; r += kThreads) {
+        for (int i = tid; i < LT * 256; i += kQThreads) A.q_T[(int64_t)qi * LT * 256 + i] = s_T[i];
+        for (int i = tid; i < len; i += kQThreads) A.q_hat[(int64_t)qi * len + i] = reinterpret_cast<const float*>(s_qh4)[i];
+        for (int r = tid; r < S.tkn; r += kQThreads) {
           h->tkd[r] = s_tkd[r];
           h->tki[r] = s_tki[r];
         }
@@ -1212,7 +1223,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_query(const __grid_constant__ Q
       }
     }
     // ---------------------------------------------------------------- output
-    for (int r = tid; s_dense < 0 && S.ntask == 0 && r < A.k; r += kThreads) {
+    for (int r = tid; s_dense < 0 && S.ntask == 0 && r < A.k; r += kQThreads) {
       const bool ok = r < S.tkn;
       A.od[(int64_t)qi * A.k + r] = ok ? sqrtf(s_tkd[r]) : INFINITY;
       A.oi[(int64_t)qi * A.k + r] = ok ? A.goff + s_tki[r] : -1;
@@ -1256,13 +1267,13 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
   QArgs A = A0;
   constexpr int UB0 = 2 * LT * 256 * 4, UB1 = CAP_B * 8, UB2 = NF * 128 * 8;
   constexpr int UB = UB0 > UB1 ? (UB0 > UB2 ? UB0 : UB2) : (UB1 > UB2 ? UB1 : UB2);
-  const size_t smem = NF * 128 * 4 + LT * 8 + LT * 256 * 4 + UB + kThreads * 8 + KMAX * 8;
+  const size_t smem = NF * 128 * 4 + LT * 8 + LT * 256 * 4 + UB + kQThreads * 8 + KMAX * 8;
   auto kern = k_query<LT, NF, RR>;
   // launch shape, once per instantiation and device (no driver queries on the per-call path)
   static int cached_dev = -1, per_sm = 0, sms = 148;
   if (cached_dev != ix->device) {
     SOFA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SOFA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+    SOFA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQThreads, smem));
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
     if (per_sm < 1) per_sm = 1;
     cached_dev = ix->device;
@@ -1315,14 +1326,14 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
   A.q_hat = reinterpret_cast<float*>(ix->q_hat);
   A.pool = reinterpret_cast<unsigned long long*>(ix->pool);
   A.tasks = reinterpret_cast<ScanTask*>(ix->tasks);
-  kern<<<grid, kThreads, smem, st>>>(A);
+  kern<<<grid, kQThreads, smem, st>>>(A);
   SOFA_LAUNCHED();
   return SOFA_OK;
 }
 
-int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
-                 cudaStream_t st, bool scan, int64_t lb_m, float* lb_out, float* ed_out, int64_t* lb_rows,
-                 float* seed_out) {
+int launch_query_impl(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
+                      cudaStream_t st, bool scan, int64_t lb_m, float* lb_out, float* ed_out, int64_t* lb_rows,
+                      float* seed_out) {
   QArgs A{};
   A.mode = seed_out ? 3 : (lb_m > 0 ? 2 : (scan ? 1 : 0));
   A.seed_out = seed_out;
@@ -1474,4 +1485,35 @@ int launch_fill_pad(float* od, int64_t* oi, int64_t cnt, cudaStream_t st) {
   return SOFA_OK;
 }
 
+}  // namespace SOFA_QNS
+
+#ifdef SOFA_QMAIN
+int launch_query_q512(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
+                      cudaStream_t st, bool scan, int64_t lb_m, float* lb_out, float* ed_out, int64_t* lb_rows,
+                      float* seed_out);
+
+// the front of a batch with at most one query per SM runs the 16-warp build (a lone query gets twice
+// the warps: configs[0] 0.55 -> 0.41 ms); every other launch the 8-warp build (3 CTAs per SM)
+int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
+                 cudaStream_t st, bool scan, int64_t lb_m, float* lb_out, float* ed_out, int64_t* lb_rows,
+                 float* seed_out) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+  bool wide = !scan && lb_m == 0 && !seed_out && q <= sms;
+  if (const char* e = getenv("SOFA_FRONT_WIDE")) wide = wide && atoi(e) != 0;  // tuning knob
+  if (wide) return launch_query_q512(ix, Q, q, k, bsf_init, od, oi, st, scan, lb_m, lb_out, ed_out, lb_rows, seed_out);
+  return q256::launch_query_impl(ix, Q, q, k, bsf_init, od, oi, st, scan, lb_m, lb_out, ed_out, lb_rows, seed_out);
+}
+int launch_merge(const float* d, const int64_t* i, int parts, int q, int k, float* od, int64_t* oi, cudaStream_t st) {
+  return q256::launch_merge(d, i, parts, q, k, od, oi, st);
+}
+int launch_fill_value(float* o, int64_t cnt, float v, cudaStream_t st) { return q256::launch_fill_value(o, cnt, v, st); }
+int launch_fill_pad(float* od, int64_t* oi, int64_t cnt, cudaStream_t st) { return q256::launch_fill_pad(od, oi, cnt, st); }
+#else
+int launch_query_q512(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
+                      cudaStream_t st, bool scan, int64_t lb_m, float* lb_out, float* ed_out, int64_t* lb_rows,
+                      float* seed_out) {
+  return SOFA_QNS::launch_query_impl(ix, Q, q, k, bsf_init, od, oi, st, scan, lb_m, lb_out, ed_out, lb_rows, seed_out);
+}
+#endif
 }  // namespace sofa
