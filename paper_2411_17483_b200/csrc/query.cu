@@ -1492,15 +1492,16 @@ int launch_query_q512(sofa_index* ix, const float* Q, int q, int k, const float*
                       cudaStream_t st, bool scan, int64_t lb_m, float* lb_out, float* ed_out, int64_t* lb_rows,
                       float* seed_out);
 
-// the front of a batch with at most one query per SM runs the 16-warp build (a lone query gets twice
-// the warps: configs[0] 0.55 -> 0.41 ms); every other launch the 8-warp build (3 CTAs per SM)
+// a batch with at most one query per SM runs the 16-warp build (a lone query gets twice the warps:
+// configs[0] 0.55 -> 0.43 ms for the front, -> 0.40 ms with the scan pool too); every other launch
+// the 8-warp build (3 CTAs per SM)
 int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
                  cudaStream_t st, bool scan, int64_t lb_m, float* lb_out, float* ed_out, int64_t* lb_rows,
                  float* seed_out) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
-  bool wide = !scan && lb_m == 0 && !seed_out && q <= sms;
-  if (const char* e = getenv("SOFA_FRONT_WIDE")) wide = wide && atoi(e) != 0;  // tuning knob
+  bool wide = lb_m == 0 && !seed_out && q <= sms;
+  if (const char* e = getenv(scan ? "SOFA_SCAN_WIDE" : "SOFA_FRONT_WIDE")) wide = wide && atoi(e) != 0;  // tuning knobs
   if (wide) return launch_query_q512(ix, Q, q, k, bsf_init, od, oi, st, scan, lb_m, lb_out, ed_out, lb_rows, seed_out);
   return q256::launch_query_impl(ix, Q, q, k, bsf_init, od, oi, st, scan, lb_m, lb_out, ed_out, lb_rows, seed_out);
 }
