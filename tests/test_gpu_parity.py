@@ -364,3 +364,21 @@ def test_revisit_pass_and_front_split(monkeypatch, rev_rounds, kind, k, front_ba
     monkeypatch.setenv("SOFA_FRONT_BATCHES", "1000000")
     d2, i2 = ix.knn(q, k)
     assert torch.equal(d, d2) and torch.equal(i, i2)
+
+
+@pytest.mark.parametrize("kind,k", [("cfg1", 1), ("cfg4", 5)])
+def test_wide_and_narrow_query_builds_agree(monkeypatch, kind, k):
+    """a batch of at most one query per SM runs the 16-warp build of the query kernels (query512.cu);
+    forcing the 8-warp build (SOFA_FRONT_WIDE=0, SOFA_SCAN_WIDE=0) must give the same bits, and both
+    equal the oracle's brute force"""
+    w = datagen.scaled(datagen.WORKLOADS[kind], 150_000 + 7, 37)
+    x, q = _data(w)
+    ix = SofaIndex(x, sample_size=3000, dense_permille=-1)
+    d, i = ix.knn(q, k)
+    monkeypatch.setenv("SOFA_FRONT_WIDE", "0")
+    monkeypatch.setenv("SOFA_SCAN_WIDE", "0")
+    d2, i2 = ix.knn(q, k)
+    torch.cuda.synchronize()
+    assert torch.equal(d, d2) and torch.equal(i, i2)
+    do, io = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), k)
+    assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, x.cpu().numpy(), q.cpu().numpy())
