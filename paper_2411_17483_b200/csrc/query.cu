@@ -1501,7 +1501,8 @@ int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
   bool wide = lb_m == 0 && !seed_out && q <= sms;
-  if (const char* e = getenv(scan ? "SOFA_SCAN_WIDE" : "SOFA_FRONT_WIDE")) wide = wide && atoi(e) != 0;  // tuning knobs
+  if (const char* e = getenv(scan ? "SOFA_SCAN_WIDE" : "SOFA_FRONT_WIDE"))  // tuning knobs: 0 never, 2 always
+    wide = atoi(e) == 2 ? lb_m == 0 && !seed_out : wide && atoi(e) != 0;
   if (wide) return launch_query_q512(ix, Q, q, k, bsf_init, od, oi, st, scan, lb_m, lb_out, ed_out, lb_rows, seed_out);
   return q256::launch_query_impl(ix, Q, q, k, bsf_init, od, oi, st, scan, lb_m, lb_out, ed_out, lb_rows, seed_out);
 }
