@@ -1,7 +1,12 @@
 #!/usr/bin/env python
 """Benchmark of the B200-native SOFA exact k-NN path (BASELINE.json metric: exact k-NN queries/sec).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl sofa|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl sofa|reference]
+
+With --gpus N > 1 and no torchrun environment (WORLD_SIZE unset), bench.py re-executes itself under
+`python -m torch.distributed.run --nproc-per-node N` (one rank per GPU) and fails if fewer than N GPUs
+are visible (SOFA_DIST_BACKEND=gloo allows N ranks on fewer GPUs: a check of the multi-rank code path,
+never a measurement).
 
 A step = one exact k-NN batch (all Q queries of the config) through libsofa's query kernel
 (a5-a8) on an index built over the synthetic dataset (a1-a4, timed separately as `build`), plus
@@ -40,7 +45,9 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="cfg2", choices=sorted(datagen.WORKLOADS))
+    # default: BASELINE.json configs[3] (100M random walks, noisy-member mix, 1-NN) — the config the metric
+    # "queries/sec at 1/2/4/8 B200" is quoted on; it fits one B200 (102.4 GB of rows + ~4 GB of index)
+    p.add_argument("--config", default="cfg4", choices=sorted(datagen.WORKLOADS))
     p.add_argument("--impl", default="sofa", choices=["sofa", "reference"])
     p.add_argument("--n-series", type=int, default=0, help="override N (debug only; changes the workload)")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -51,6 +58,36 @@ def parse():
 
 
 TF32_PER_BF16 = 1.1 / 2.25  # nominal dense TF32 : BF16 tensor throughput (B200_PROFILING.md)
+HBM_NOMINAL_GBS = 8000.0    # BASELINE.json north_star "roughly 8 TB/s" (DGX figure; HGX 7.7)
+
+
+def lib_fingerprint() -> str | None:
+    p = os.path.join(ROOT, "paper_2411_17483_b200", "lib", "libsofa.sha256")
+    return open(p).read().strip() if os.path.exists(p) else None
+
+
+def load_traffic(config: str) -> dict | None:
+    """profiles/traffic_<config>.json: DRAM bytes per step of each kernel group from an ncu capture
+    (tools/traffic.py), valid only for the library build it was captured on."""
+    tp = os.path.join(ROOT, "profiles", f"traffic_{config}.json")
+    if not os.path.exists(tp):
+        return None
+    d = json.load(open(tp))
+    if d.get("lib_fingerprint") != lib_fingerprint():
+        return None
+    return d.get("groups")
+
+
+def dense_roofline(st, km, rows, w, bf16, bf16_kind):
+    """dense pass (f1): 2 * queries * rows * n flops of the screen GEMM (the exact refine is tiny)"""
+    flops = 2.0 * st["dense_queries"] * rows * w.length
+    tf32_peak = bf16 * TF32_PER_BF16
+    dn = {"bound": "tensor", "achieved": flops / (km["dense"] / 1e3) / 1e12, "peak": tf32_peak, "unit": "TFLOP/s",
+          "kernel": "k_dense_screen + k_dense_post (tcgen05 kind::tf32)", "group": "dense", "kernel_ms": km["dense"],
+          "algorithmic_flops_per_launch": flops,
+          "peak_note": f"{bf16_kind} {bf16:.1f} TFLOP/s x 1.1/2.25 (nominal dense TF32/BF16 ratio)"}
+    dn["frac"] = dn["achieved"] / tf32_peak
+    return dn
 
 
 def peaks():
@@ -175,8 +212,26 @@ def flush_l2(buf):
     buf.zero_()
 
 
+def self_launch(a):
+    """--gpus N > 1 without a torchrun environment: re-exec under torch.distributed.run (N ranks)."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    if a.impl != "reference" and os.environ.get("SOFA_DIST_BACKEND", "nccl") == "nccl":
+        have = torch.cuda.device_count()
+        if have < a.gpus:
+            sys.exit(f"bench.py: --gpus {a.gpus} needs {a.gpus} visible GPUs, found {have}")
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     a = parse()
+    self_launch(a)
     w = datagen.WORKLOADS[a.config]
     if a.n_series:
         w = datagen.scaled(w, a.n_series, w.n_queries)
@@ -288,25 +343,28 @@ def main():
                     + st["queries"] * n_b)
     sparse_ms = km["front"] + km["scan"]
     sparse = {"bound": "hbm", "achieved": sparse_bytes / (sparse_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
-              "kernel": "k_query front + scan (a5-a8)", "kernel_ms": sparse_ms, "algorithmic_bytes_per_launch": sparse_bytes}
+              "kernel": "k_query front + scan (a5-a8)", "group": "sparse", "kernel_ms": sparse_ms,
+              "algorithmic_bytes_per_launch": sparse_bytes}
     sparse["frac"] = sparse["achieved"] / hbm
+    # report against both the measured copy rate and the north star's ~8 TB/s nominal
+    sparse["peak_nominal"] = HBM_NOMINAL_GBS
+    sparse["frac_nominal"] = sparse["achieved"] / HBM_NOMINAL_GBS
     rooflines = [sparse]
     if st["dense_queries"] > 0 and km["dense"] > 0:
-        # dense pass: 2 * queries * rows * n flops of the TF32 GEMM (the exact refine is tiny)
-        flops = 2.0 * st["dense_queries"] * (hi - lo) * w.length
-        tf32_peak = bf16 * TF32_PER_BF16
-        dn = {"bound": "tensor", "achieved": flops / (km["dense"] / 1e3) / 1e12, "peak": tf32_peak, "unit": "TFLOP/s",
-              "kernel": "k_dense_screen + k_dense_post (tcgen05 kind::tf32)", "kernel_ms": km["dense"],
-              "algorithmic_flops_per_launch": flops,
-              "peak_note": f"{bf16_kind} {bf16:.1f} TFLOP/s x 1.1/2.25 (nominal dense TF32/BF16 ratio)"}
-        dn["frac"] = dn["achieved"] / tf32_peak
-        rooflines.append(dn)
+        rooflines.append(dense_roofline(st, km, hi - lo, w, bf16, bf16_kind))
+    # DRAM bytes per step of each group, from the ncu capture of THIS build (the library fingerprint
+    # must match, else the number is from other kernels and is not reported)
+    traffic = load_traffic(a.config)
+    for r in rooflines:
+        tb = traffic.get(r["group"]) if traffic else None
+        r["dram_bytes_per_launch"] = tb
+        if tb:
+            r["dram_gbs"] = tb / (r["kernel_ms"] / 1e3) / 1e9
+            r["dram_frac"] = r["dram_gbs"] / hbm
+            r["dram_frac_nominal"] = r["dram_gbs"] / HBM_NOMINAL_GBS
     dominant = max(rooflines, key=lambda r: r["kernel_ms"])
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{a.config}.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-    roofline = dict(dominant, traffic=traffic, peak_kind=peak_kind, share_of_step=dominant["kernel_ms"] / sum(km.values()))
+    roofline = dict(dominant, traffic=dominant.get("dram_bytes_per_launch"), peak_kind=peak_kind,
+                    share_of_step=dominant["kernel_ms"] / sum(km.values()))
 
     # ---------------------------------------------------------------- e2e through the host C call
     e2e = None

@@ -122,6 +122,28 @@ typedef struct {
                                dense pass (screen + exact refine) and the scan kernel */
 } sofa_knn_stats;
 
+/* Per-index tuning of the query kernels (read once by sofa_set_tuning, never from the environment).
+ * Every field changes only the ORDER of work or which kernel build runs, never a result (the
+ * tests check bit-identical outputs across settings).  sofa_default_tuning gives the defaults. */
+typedef struct {
+  int32_t front_batches;   /* word batches of LB-ordered leaves the front scans per query before the
+                              rest becomes scan tasks (default 16; >= 1) */
+  int32_t rev_rounds;      /* refine rounds of a leaf part before it is deferred to the revisit pass
+                              (default 2; 0 defers every part with a candidate) */
+  int32_t topm_min;        /* top-M seeding for leaf lists longer than this (0 => nb/16 clamped to
+                              [256, 2048]) */
+  int32_t topm_leaves;     /* top-M seeding over about this many lowest-LB leaves (default 64) */
+  int32_t refine_rows_front; /* rows refined together per warp in the front: 0 auto, 2 or 4 (n <= 512) */
+  int32_t refine_rows_scan;  /* the same for the scan pool: 0 auto (2), 2 or 4 */
+  int32_t front_wide;      /* 16-warp build of the front: -1 auto (batches of at most one query per
+                              SM), 0 never, 1 always */
+  int32_t scan_wide;       /* the same for the scan pool */
+  int64_t dense_cand_cap;  /* dense-path candidate buffer entries (0 => 16M); a query whose candidates
+                              overflow it is rescanned brute force (testing) */
+} sofa_tuning;
+
+int sofa_default_tuning(sofa_tuning* out);
+
 /* Fill *out with defaults (sample_ratio 0.01, block_size 256, equi-depth, everything else 0). */
 int sofa_default_opts(sofa_build_opts* out);
 
@@ -202,6 +224,9 @@ int sofa_knn_trace(const sofa_index* ix, int64_t* out_host, int32_t q);
  *   (global row index of column j).  All device pointers.  Errors: EINVAL, ECUDA. */
 int sofa_lower_bounds(sofa_index* ix, const float* queries_dev, int32_t q, int64_t m, float* out_lb2_dev,
                       float* out_ed2_dev, int64_t* out_rows_dev, void* cuda_stream);
+
+/* Replace the index's query tuning (host struct, copied).  Errors: EINVAL (NULL, out of range). */
+int sofa_set_tuning(sofa_index* ix, const sofa_tuning* t);
 
 /* Copy the index's model to *out (host). */
 int sofa_get_model(const sofa_index* ix, sofa_model* out);

@@ -22,6 +22,8 @@ What each part computes (and what pins it, tests/test_oracle.py):
   lb_envelope      leaf LB of a block, reading 10           pinned: env LB <= member LB
   knn_bruteforce   NN definition (reading 14), k-NN       pinned: pure-python loops,
                                                                          noisy-member known answers
+  knn_bruteforce_stream  the same, over row chunks (torch CPU float64)  pinned: == pure-python loops,
+                                                                         chunk-boundary ties
   knn_gemini       GEMINI filter+refine              pinned: == brute force
   paa / isax_*     the iSAX baseline: PAA segments, N(0,1)  pinned: textbook breakpoints,
                    breakpoints, mindist weight n/l                      PAA closed forms, LB <= ED^2
@@ -296,6 +298,70 @@ def knn_bruteforce(data: np.ndarray, queries: np.ndarray, k: int, chunk: int = 1
     for q in range(nq):
         best_d[q, :kk] = np.sqrt(cand_d[q])
         best_i[q, :kk] = cand_i[q]
+    return best_d, best_i
+
+
+def knn_bruteforce_stream(chunks, queries: np.ndarray, k: int, rows_per_gemm: int = 1 << 17):
+    """knn_bruteforce over a dataset too large for host memory, read as consecutive row chunks.
+
+    The same definition (P:96 with reading 14; k-NN P:177) and the same two steps as
+    knn_bruteforce — a float64 norm-expansion GEMM that only shortlists, then exact float64
+    direct sums — written with torch CPU float64 ops so a 10^8-row dataset is checked in
+    minutes on the host's cores.  `chunks` yields (first_row, float32 array) in row order.
+    Shortlist rule per query: expanded d^2 <= (the running exact k-th best, or, while fewer than
+    k rows are known, the chunk's own k-th smallest expanded d^2) + margin, with the margin of
+    knn_bruteforce (far above the expansion's error).  A row of the final top-k has expanded
+    d^2 <= its exact d^2 + err <= the running k-th best + err, so it is always shortlisted.
+    Returns (dist (Q,k) = sqrt(d^2), idx (Q,k) int64), padded with (+inf, -1).
+    """
+    import torch
+
+    qh = torch.from_numpy(znorm(np.atleast_2d(queries))[0])          # float64, Q x n
+    nq, n = qh.shape
+    qn = (qh * qh).sum(dim=1)
+    cand_d = [np.empty(0)] * nq
+    cand_i = [np.empty(0, dtype=np.int64)] * nq
+    kth = np.full(nq, np.inf)                                        # running exact k-th best d^2
+    for first, data in chunks:
+        data = np.asarray(data)
+        for s in range(0, data.shape[0], rows_per_gemm):
+            x = torch.from_numpy(np.ascontiguousarray(data[s:s + rows_per_gemm])).to(torch.float64)
+            # z-norm (Def. 2, population std, reading 1), same arithmetic as znorm()
+            mu = x.mean(dim=1, keepdim=True)
+            x -= mu
+            sd = (x * x).mean(dim=1, keepdim=True).sqrt()
+            flag = sd < 1e-12
+            x /= torch.where(flag, torch.ones_like(sd), sd)
+            x[flag[:, 0]] = 0.0
+            xn = (x * x).sum(dim=1)
+            approx = qn[:, None] + xn[None, :] - 2.0 * (qh @ x.T)
+            margin = 1e-9 * n + 64 * n * 2.0 ** -52 * float(torch.sqrt(qn.max() * xn.max()))
+            thr = torch.from_numpy(kth.copy())
+            open_q = np.nonzero(~np.isfinite(kth))[0]
+            if len(open_q):                                          # fewer than k rows known yet
+                kk = min(k, approx.shape[1])
+                ck = torch.kthvalue(approx[open_q], kk, dim=1).values
+                thr[open_q] = torch.minimum(thr[open_q], ck)
+            qs, cols = torch.nonzero(approx <= (thr + margin)[:, None], as_tuple=True)
+            if len(qs) == 0:
+                continue
+            qs, cols = qs.numpy(), cols.numpy()
+            diff = x[cols] - qh[qs]
+            d2 = (diff * diff).sum(dim=1).numpy()                    # exact direct sums (P:93)
+            for q in np.unique(qs):
+                sel = qs == q
+                cd = np.concatenate([cand_d[q], d2[sel]])
+                ci = np.concatenate([cand_i[q], cols[sel] + first + s])
+                cd, ci = _topk(cd, ci, k)
+                cand_d[q], cand_i[q] = cd, ci
+                if len(cd) >= k:
+                    kth[q] = cd[k - 1]
+    best_d = np.full((nq, k), np.inf)
+    best_i = np.full((nq, k), -1, dtype=np.int64)
+    for q in range(nq):
+        m = len(cand_d[q])
+        best_d[q, :m] = np.sqrt(cand_d[q])
+        best_i[q, :m] = cand_i[q]
     return best_d, best_i
 
 

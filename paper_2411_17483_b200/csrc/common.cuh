@@ -154,6 +154,27 @@ __device__ __forceinline__ void ed_warp_multi(const float* const (&rows)[R], con
   }
 }
 
+// One query's result (a8 -> caller), written by ONE thread.  The top-k is kept sorted by (d^2, row);
+// the caller's order is (d, global index) with d = sqrtf(d^2) (include/sofa.h), which differs only
+// where distinct d^2 round to the same d: an insertion pass (k <= 128, almost always a no-op) puts
+// those runs in index order, so every writer — and the cross-shard merge (a9), which only sees d —
+// agrees on one order.  Missing entries pad with (+inf, -1).
+__device__ __forceinline__ void write_topk(const volatile float* td, const volatile int* ti, int n, int k,
+                                           int64_t goff, float* __restrict__ od, int64_t* __restrict__ oi) {
+  for (int r = 0; r < k; ++r) {
+    const float d = r < n ? sqrtf(td[r]) : INFINITY;
+    const int64_t i = r < n ? goff + ti[r] : -1;
+    int p = r;
+    while (p > 0 && i >= 0 && od[p - 1] == d && oi[p - 1] > i) {
+      od[p] = od[p - 1];
+      oi[p] = oi[p - 1];
+      --p;
+    }
+    od[p] = d;
+    oi[p] = i;
+  }
+}
+
 // upper_bound over a 256-entry edge row padded with +inf: number of edges <= v (symbol of v;
 // bins [beta(s), beta(s+1)) — P:225-228, value on an edge goes right).
 template <typename E>
@@ -279,6 +300,8 @@ struct sofa_index {
   int64_t* hi_dev = nullptr;
   int64_t h_cap = 0;
   int device = 0;
+  int sms = 148;        // multiprocessors of `device` (queried once at build time)
+  sofa_tuning tune{};   // query-kernel tuning (sofa_set_tuning; defaults from sofa_default_tuning)
   sofa::DevModel dm{};
 };
 

@@ -536,13 +536,10 @@ __global__ void __launch_bounds__(kThreads) k_dense_post(const DensePost P) {
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int64_t e = threadIdx.x; e < (int64_t)qd * P.k; e += kThreads) {
-    const int slot = (int)(e / P.k), r = (int)(e % P.k);
+  for (int slot = threadIdx.x; slot < qd; slot += kThreads) {
     const int qi = P.qidx[slot];
-    const int n = *(volatile int*)&P.tkn[slot];
-    const bool ok = r < n;
-    P.od[(int64_t)qi * P.k + r] = ok ? sqrtf(*(volatile float*)&P.tkd[(int64_t)slot * P.k + r]) : INFINITY;
-    P.oi[(int64_t)qi * P.k + r] = ok ? P.goff + *(volatile int*)&P.tki[(int64_t)slot * P.k + r] : -1;
+    write_topk(P.tkd + (int64_t)slot * P.k, P.tki + (int64_t)slot * P.k, *(volatile int*)&P.tkn[slot], P.k, P.goff,
+               P.od + (int64_t)qi * P.k, P.oi + (int64_t)qi * P.k);
   }
   if (threadIdx.x == 0 && P.dstats) {
     atomicAdd(&P.dstats[19], (unsigned long long)qd);
@@ -613,11 +610,12 @@ int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stat
   A.ovf_count = D.counters + 1;
   A.progress = D.counters + 64;
   auto screen = k == 1 ? k_dense_screen<true> : k_dense_screen<false>;
-  static int cached_dev[2] = {-1, -1}, sms = 148;
-  if (cached_dev[k == 1] != ix->device) {
+  const int sms = ix->sms;
+  static std::atomic<uint32_t> attr_set{0};  // per (device, k == 1): smem attribute set once
+  const uint32_t bit = 1u << ((ix->device * 2 + (k == 1)) & 31);
+  if (!(attr_set.load() & bit)) {
     SOFA_CK(cudaFuncSetAttribute(screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D_SMEM));
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
-    cached_dev[k == 1] = ix->device;
+    attr_set.fetch_or(bit);
   }
   screen<<<sms, D_THREADS, D_SMEM, st>>>(tmQ, tmX, A);
   SOFA_LAUNCHED();
@@ -674,8 +672,7 @@ int ensure_dense_scratch(sofa_index* ix, int q, int k) {
   D.q_cap = q;
   D.k_cap = k;
   D.len = ix->len;
-  D.cand_cap = (int64_t)16 << 20;
-  if (const char* e = getenv("SOFA_DENSE_CAND_CAP")) D.cand_cap = atoll(e) > 0 ? atoll(e) : 1;  // test knob
+  D.cand_cap = ix->tune.dense_cand_cap > 0 ? ix->tune.dense_cand_cap : (int64_t)16 << 20;
   SOFA_CK(cudaMalloc(&D.qhat, (size_t)q * ix->len * 4));
   SOFA_CK(cudaMalloc(&D.qparams, (size_t)q * 16));
   SOFA_CK(cudaMalloc(&D.qidx, (size_t)q * 4));

@@ -24,8 +24,6 @@
 // exceeds the query's BSF is rejected unread; the CTA finishing a query's last task writes it.
 // thr = BSF * (1 + 1e-4) + 1e-5 (squared units): prune only when the float32 lower bound clearly
 // exceeds the float32 k-th best; this absorbs the data-side projection error (reading 15).
-#include <cstdlib>
-
 #include "common.cuh"
 
 // This file is compiled twice: as itself (8-warp CTAs, 3 per SM: batches with several queries per
@@ -166,7 +164,7 @@ __device__ __forceinline__ void warp_append(bool pass, unsigned long long key, u
 }
 
 struct QShared {
-  int qi, cnt, tkn, take, rem, next, lock, gslot, chunk, ntask, nrev;
+  int qi, cnt, tkn, take, rem, next, lock, gslot, chunk, chsz, ntask, nrev;
   long long off;
   float bsf, bsf_init, thr;
   // per query: 0 blocks_survived, 1 words_scanned, 2 candidates, 3 refined, 4 abandoned, 5 env_nodes,
@@ -472,16 +470,24 @@ __device__ void publish_tasks(const QArgs& A, QShared& S, int q, const unsigned 
                               bool dense_cand) {
   if (n <= 0) return;
   const int tid = threadIdx.x;
-  const int CH = chunk_blocks<LT>(A.B);
-  const int nt = (n + CH - 1) / CH;
   const int set = dense_cand ? 1 : 0;
   if (tid == 0) {
+    // ranks left for this query (rank_cap covers ceil(nb / CH) + 2 ranks; a query publishes at most
+    // twice, so this never binds today): if the list needed more, its chunks grow instead of being
+    // dropped — every published task is stored, so the query's done counter always reaches ntasks
+    int CH = chunk_blocks<LT>(A.B);
+    const int left = A.rank_cap - S.ntask;
+    if (left <= 0) __trap();
+    if ((n + CH - 1) / CH > left) CH = (n + left - 1) / left;
+    S.chsz = CH;
     S.off = (long long)atomicAdd(A.pool_used, (unsigned long long)n);
     S.chunk = S.ntask;
-    S.ntask += nt;
+    S.ntask += (n + CH - 1) / CH;
     atomicMax(&A.counters[2 * set], S.ntask);
   }
   __syncthreads();
+  const int CH = S.chsz;
+  const int nt = (n + CH - 1) / CH;
   const int64_t off = S.off;
   const int r0 = S.chunk;
   for (int i = tid; i < n; i += kQThreads) A.pool[off + i] = list[i];
@@ -493,8 +499,8 @@ __device__ void publish_tasks(const QArgs& A, QShared& S, int q, const unsigned 
     t.off = off + (int64_t)i * CH;
     t.q = q;
     t.cnt_flags = (n - i * CH < CH ? n - i * CH : CH) | flags;
-    const int r = r0 + i;
-    if (r < A.rank_cap) tasks[(int64_t)r * A.q + atomicAdd(&rc[r], 1)] = t;
+    const int r = r0 + i;  // < rank_cap by the CH choice above
+    tasks[(int64_t)r * A.q + atomicAdd(&rc[r], 1)] = t;
   }
   __syncthreads();
 }
@@ -576,14 +582,8 @@ __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd,
       S.gslot = -1;
     }
     __syncthreads();
-    if (S.take) {  // last task of this query: write its result
-      const int n = h->tkn;
-      for (int r = tid; r < A.k; r += kQThreads) {
-        const bool ok = r < n;
-        A.od[(int64_t)q * A.k + r] = ok ? sqrtf(h->tkd[r]) : INFINITY;
-        A.oi[(int64_t)q * A.k + r] = ok ? A.goff + h->tki[r] : -1;
-      }
-    }
+    if (S.take && tid == 0)  // last task of this query: write its result
+      write_topk(h->tkd, h->tki, h->tkn, A.k, A.goff, A.od + (int64_t)q * A.k, A.oi + (int64_t)q * A.k);
     __syncthreads();
   }
   if (tid == 0 && A.dstats)
@@ -1223,11 +1223,8 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
       }
     }
     // ---------------------------------------------------------------- output
-    for (int r = tid; s_dense < 0 && S.ntask == 0 && r < A.k; r += kQThreads) {
-      const bool ok = r < S.tkn;
-      A.od[(int64_t)qi * A.k + r] = ok ? sqrtf(s_tkd[r]) : INFINITY;
-      A.oi[(int64_t)qi * A.k + r] = ok ? A.goff + s_tki[r] : -1;
-    }
+    if (s_dense < 0 && S.ntask == 0 && tid == 0)
+      write_topk(s_tkd, s_tki, S.tkn, A.k, A.goff, A.od + (int64_t)qi * A.k, A.oi + (int64_t)qi * A.k);
     t_phase[4] = clock64();
     if (tid == 0 && A.dstats) {
       atomicAdd(&A.dstats[0], 1ull);
@@ -1269,15 +1266,18 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
   constexpr int UB = UB0 > UB1 ? (UB0 > UB2 ? UB0 : UB2) : (UB1 > UB2 ? UB1 : UB2);
   const size_t smem = NF * 128 * 4 + LT * 8 + LT * 256 * 4 + UB + kQThreads * 8 + KMAX * 8;
   auto kern = k_query<LT, NF, RR>;
-  // launch shape, once per instantiation and device (no driver queries on the per-call path)
-  static int cached_dev = -1, per_sm = 0, sms = 148;
-  if (cached_dev != ix->device) {
+  // launch shape, once per instantiation and device (no driver queries on the per-call path; racing
+  // first calls set the same attribute and store the same value)
+  static std::atomic<int> per_sm_cache[16];
+  std::atomic<int>& slot = per_sm_cache[ix->device & 15];
+  int per_sm = slot.load();
+  if (per_sm == 0) {
     SOFA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     SOFA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQThreads, smem));
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
     if (per_sm < 1) per_sm = 1;
-    cached_dev = ix->device;
+    slot.store(per_sm);
   }
+  const int sms = ix->sms;
   // the whole GPU even for a small batch: CTAs without a query of their own help heavy ones
   const int grid = sms * per_sm;
   const int64_t need = (int64_t)grid * 2 * (ix->nb > 0 ? ix->nb : 1);
@@ -1341,16 +1341,14 @@ int launch_query_impl(sofa_index* ix, const float* Q, int q, int k, const float*
   A.lb_out = lb_out;
   A.ed_out = ed_out;
   A.lb_rows = lb_rows;
-  A.front_batches = 16;
-  if (const char* e = getenv("SOFA_FRONT_BATCHES")) A.front_batches = atoi(e) > 0 ? atoi(e) : 1;  // tuning knob
-  A.rev_rounds = 2;
-  if (const char* e = getenv("SOFA_REV_ROUNDS")) A.rev_rounds = atoi(e);  // tuning knob
+  const sofa_tuning& T = ix->tune;
+  A.front_batches = T.front_batches > 0 ? T.front_batches : 16;
+  A.rev_rounds = T.rev_rounds;
   // top-M seeding only for lists longer than ~1/16 of the index, in [TOPM_MIN_LEAVES, CAP_B] leaves: a
   // shorter list is cheaper to scan in LB order directly (configs[1]: 0.64 -> 0.61 ms at 2048)
-  A.topm_min = (int)(ix->nb / 16 < TOPM_MIN_LEAVES ? TOPM_MIN_LEAVES : (ix->nb / 16 > CAP_B ? CAP_B : ix->nb / 16));
-  A.topm_leaves = TOPM_LEAVES;
-  if (const char* e = getenv("SOFA_TOPM_MIN")) A.topm_min = atoi(e);  // tuning knobs
-  if (const char* e = getenv("SOFA_TOPM_LEAVES")) A.topm_leaves = atoi(e) > 0 ? (atoi(e) < CAP_B ? atoi(e) : CAP_B) : 1;
+  A.topm_min = T.topm_min > 0 ? T.topm_min
+                              : (int)(ix->nb / 16 < TOPM_MIN_LEAVES ? TOPM_MIN_LEAVES : (ix->nb / 16 > CAP_B ? CAP_B : ix->nb / 16));
+  A.topm_leaves = T.topm_leaves > 0 ? (T.topm_leaves < CAP_B ? T.topm_leaves : CAP_B) : TOPM_LEAVES;
   A.series = ix->series;
   A.n = ix->n;
   A.nb = ix->nb;
@@ -1407,10 +1405,10 @@ int launch_query_impl(sofa_index* ix, const float* Q, int q, int k, const float*
   // queries, configs[1] 0.57 vs 0.62 ms) or, for n <= 256 and at most one query per CTA, 4 (more row
   // loads in flight per warp: a batch that small is set by its slowest, refine-bound query;
   // configs[0] 0.55 vs 0.63 ms).  The scan pool is indifferent (measured) and uses 2.
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+  const int sms = ix->sms;
   int rsel = A.mode == 0 && A.q <= 3 * sms ? 4 : 2;
-  if (const char* e = getenv(A.mode == 1 ? "SOFA_R_SCAN" : "SOFA_R_FRONT")) rsel = atoi(e);  // tuning knobs
+  const int rt = A.mode == 1 ? T.refine_rows_scan : T.refine_rows_front;
+  if (rt) rsel = rt;
 #define SOFA_Q(lt, nf) \
   if (ix->LT == lt && NF == nf) {                                                       \
     if (nf <= 2 && rsel == 4) return launch_query_t<lt, (nf <= 2 ? nf : 1), 4>(ix, A, st); \
@@ -1498,11 +1496,8 @@ int launch_query_q512(sofa_index* ix, const float* Q, int q, int k, const float*
 int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
                  cudaStream_t st, bool scan, int64_t lb_m, float* lb_out, float* ed_out, int64_t* lb_rows,
                  float* seed_out) {
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
-  bool wide = lb_m == 0 && !seed_out && q <= sms;
-  if (const char* e = getenv(scan ? "SOFA_SCAN_WIDE" : "SOFA_FRONT_WIDE"))  // tuning knobs: 0 never, 2 always
-    wide = atoi(e) == 2 ? lb_m == 0 && !seed_out : wide && atoi(e) != 0;
+  const int wt = scan ? ix->tune.scan_wide : ix->tune.front_wide;  // -1 auto, 0 never, 1 always
+  const bool wide = lb_m == 0 && !seed_out && (wt == 1 || (wt == -1 && q <= ix->sms));
   if (wide) return launch_query_q512(ix, Q, q, k, bsf_init, od, oi, st, scan, lb_m, lb_out, ed_out, lb_rows, seed_out);
   return q256::launch_query_impl(ix, Q, q, k, bsf_init, od, oi, st, scan, lb_m, lb_out, ed_out, lb_rows, seed_out);
 }

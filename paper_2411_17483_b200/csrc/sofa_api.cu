@@ -162,6 +162,39 @@ int sofa_kernel_timing(sofa_index* ix, int32_t enable, double* out_ms, int64_t* 
   return SOFA_OK;
 }
 
+int sofa_default_tuning(sofa_tuning* out) {
+  if (!out) return fail(SOFA_EINVAL, "out is NULL");
+  memset(out, 0, sizeof(*out));
+  out->front_batches = 16;
+  out->rev_rounds = 2;
+  out->topm_min = 0;
+  out->topm_leaves = 64;
+  out->refine_rows_front = 0;
+  out->refine_rows_scan = 0;
+  out->front_wide = -1;
+  out->scan_wide = -1;
+  out->dense_cand_cap = 0;
+  return SOFA_OK;
+}
+
+int sofa_set_tuning(sofa_index* ix, const sofa_tuning* t) {
+  g_err.clear();
+  if (!ix || !t) return fail(SOFA_EINVAL, "NULL pointer");
+  if (t->front_batches < 1) return fail(SOFA_EINVAL, "front_batches must be >= 1");
+  if (t->rev_rounds < 0) return fail(SOFA_EINVAL, "rev_rounds must be >= 0");
+  if (t->topm_min < 0 || t->topm_leaves < 1 || t->topm_leaves > 2048)
+    return fail(SOFA_EINVAL, "topm_min >= 0 and topm_leaves in [1, 2048]");
+  for (int r : {t->refine_rows_front, t->refine_rows_scan})
+    if (r != 0 && r != 2 && r != 4) return fail(SOFA_EINVAL, "refine_rows must be 0, 2 or 4");
+  for (int w : {t->front_wide, t->scan_wide})
+    if (w < -1 || w > 1) return fail(SOFA_EINVAL, "front_wide / scan_wide must be -1, 0 or 1");
+  if (t->dense_cand_cap < 0) return fail(SOFA_EINVAL, "dense_cand_cap must be >= 0");
+  const bool regrow = t->dense_cand_cap != ix->tune.dense_cand_cap;
+  ix->tune = *t;
+  if (regrow) free_dense_scratch(ix);  // reallocated at the next sofa_knn with the new capacity
+  return SOFA_OK;
+}
+
 int sofa_default_opts(sofa_build_opts* out) {
   if (!out) return fail(SOFA_EINVAL, "out is NULL");
   memset(out, 0, sizeof(*out));
@@ -231,6 +264,9 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
   ix->series = series_dev;
   ix->dense_permille = opts.dense_permille == 0 ? 100 : (opts.dense_permille < 0 ? 0 : opts.dense_permille);
   cudaGetDevice(&ix->device);
+  cudaDeviceGetAttribute(&ix->sms, cudaDevAttrMultiProcessorCount, ix->device);
+  if (ix->sms < 1) ix->sms = 1;
+  sofa_default_tuning(&ix->tune);
   auto bail = [&](int code) {
     sofa_free(ix);
     return code;

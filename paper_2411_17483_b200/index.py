@@ -37,6 +37,16 @@ class SofaIndex:
         self.k_max = S.MAX_K
         self._host_bufs = {}
 
+    def set_tuning(self, **fields):
+        """Query-kernel tuning (sofa_set_tuning; include/sofa.h sofa_tuning): fields not given keep
+        their defaults.  Changes the order of work only, never a result."""
+        t = S.sofa_default_tuning()
+        for kk, v in fields.items():
+            if kk not in dict(t._fields_):
+                raise KeyError(kk)
+            setattr(t, kk, int(v))
+        S.sofa_set_tuning(self.handle, t)
+
     # -------------------------------------------------------------------------------- queries
     def knn(self, queries: torch.Tensor, k: int = 1, bsf_init: torch.Tensor | None = None, stats: bool = False,
             out=None, stream=None):

@@ -54,6 +54,12 @@ class sofa_build_opts(C.Structure):
                 ("global_offset", C.c_int64), ("global_n", C.c_int64), ("model", C.POINTER(sofa_model))]
 
 
+class sofa_tuning(C.Structure):
+    _fields_ = [(f, C.c_int32) for f in ("front_batches", "rev_rounds", "topm_min", "topm_leaves",
+                                         "refine_rows_front", "refine_rows_scan", "front_wide", "scan_wide")] + \
+        [("dense_cand_cap", C.c_int64)]
+
+
 class sofa_knn_stats(C.Structure):
     _fields_ = [(f, C.c_int64) for f in ("queries", "blocks_total", "blocks_survived", "words_scanned",
                                          "candidates", "refined", "abandoned", "env_nodes", "list_blocks",
@@ -91,6 +97,8 @@ def lib() -> C.CDLL:
         L.sofa_launch_count.restype = I64
         L.sofa_kernel_timing.argtypes = [VP, I32, VP, P(I64)]
         L.sofa_default_opts.argtypes = [P(sofa_build_opts)]
+        L.sofa_default_tuning.argtypes = [P(sofa_tuning)]
+        L.sofa_set_tuning.argtypes = [VP, P(sofa_tuning)]
         L.sofa_learn_model.argtypes = [VP, I64, I32, I32, I32, P(sofa_build_opts), VP, P(sofa_model)]
         L.sofa_build.argtypes = [VP, I64, I32, I32, I32, P(sofa_build_opts), VP, P(VP)]
         L.sofa_knn.argtypes = [VP, VP, I32, I32, VP, VP, VP, P(sofa_knn_stats), VP]
@@ -150,6 +158,16 @@ def sofa_default_opts() -> sofa_build_opts:
     o = sofa_build_opts()
     _ck(lib().sofa_default_opts(C.byref(o)))
     return o
+
+
+def sofa_default_tuning() -> sofa_tuning:
+    t = sofa_tuning()
+    _ck(lib().sofa_default_tuning(C.byref(t)))
+    return t
+
+
+def sofa_set_tuning(ix, tuning: sofa_tuning):
+    _ck(lib().sofa_set_tuning(ix, C.byref(tuning)))
 
 
 def sofa_learn_model(sample_dev, S, len_, l, alphabet, opts=None, stream=None) -> sofa_model:

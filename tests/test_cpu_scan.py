@@ -5,6 +5,8 @@ import cpu_scan
 from oracle import sofa_oracle as O
 from paper_2411_17483_b200 import datagen
 
+from knn_check import assert_knn_parity
+
 
 def test_cpu_scan_equals_oracle():
     w = datagen.scaled(datagen.WORKLOADS["cfg1"], 20_000, 12, length=256)
@@ -14,7 +16,6 @@ def test_cpu_scan_equals_oracle():
     st = cpu_scan.row_stats(x)
     d, i = cpu_scan.knn(x, st, q, 5, threads=4)
     do, io = O.knn_bruteforce(x, q, 5)
-    np.testing.assert_allclose(d, do, rtol=1e-4)
-    assert (i == io).mean() > 0.99
+    assert_knn_parity(d, i, do, io, x, q)
     d1, i1 = cpu_scan.knn(x, st, x[[3]], 2, threads=3)
     assert list(i1[0]) == [3, 7] and d1[0, 0] == 0.0

@@ -3,8 +3,6 @@ inputs.  Acceptance (BASELINE.json north_star): neighbour indices exact except t
 relative distance; distances within 1e-4 relative; SFA symbols bit-exact except values within
 1e-5 of a bin edge; the learned model equal to the oracle's (best_l identical, edges within
 float32 rounding)."""
-import math
-
 import numpy as np
 import pytest
 import torch
@@ -15,34 +13,13 @@ from paper_2411_17483_b200.index import SofaIndex, learn_model, merge_topk, tran
 
 pytestmark = pytest.mark.gpu
 
-DIST_RTOL = 1e-4
-TIE_RTOL = 1e-5
+from knn_check import DIST_RTOL, TIE_RTOL, assert_knn_parity  # noqa: F401  (re-exported to the other GPU tests)
 
 
 def _data(w, device="cuda"):
     x = datagen.generate_rows(w, 0, w.n_series, device=device)
     q = datagen.generate_queries(w, device=device, data=x)
     return x, q
-
-
-def assert_knn_parity(d_gpu, i_gpu, d_or, i_or, data_np=None, queries_np=None):
-    """indices exact except ties within TIE_RTOL; distances within DIST_RTOL relative."""
-    d_gpu = np.asarray(d_gpu, dtype=np.float64)
-    assert d_gpu.shape == d_or.shape
-    fin = np.isfinite(d_or)
-    assert np.array_equal(np.isfinite(d_gpu), fin)
-    np.testing.assert_allclose(d_gpu[fin], d_or[fin], rtol=DIST_RTOL, atol=1e-6)
-    bad = (i_gpu != i_or) & fin
-    for q, r in zip(*np.nonzero(bad)):
-        # allowed only as a tie: the GPU's neighbour is within TIE_RTOL of the oracle's rank-r distance
-        ref = d_or[q, r]
-        if data_np is not None:
-            xh, _, _, _ = O.znorm(data_np[i_gpu[q, r]:i_gpu[q, r] + 1])
-            qh, _, _, _ = O.znorm(queries_np[q:q + 1])
-            true_d = math.sqrt(O.sq_dists_direct(xh, qh[0])[0])
-        else:
-            true_d = d_gpu[q, r]
-        assert abs(true_d - ref) <= TIE_RTOL * max(ref, 1e-12) + 1e-7, (q, r, i_gpu[q, r], i_or[q, r], true_d, ref)
 
 
 # ------------------------------------------------------------------------------------- a2 model
@@ -160,13 +137,17 @@ def test_result_invariant_to_block_size(B):
 
 @pytest.mark.parametrize("parts", [2, 3, 5])
 def test_sharded_merge_equals_unsharded(parts):
+    """a9: per-shard indices (global model, global offsets) + the merge kernel equal the single index
+    bit for bit AND the oracle: the merge against O.merge_topk of the oracle's per-shard lists, the
+    merged result against the oracle's brute force over all rows"""
     w = datagen.scaled(datagen.WORKLOADS["cfg1"], 30_011, 40)
     x, q = _data(w)
     k = 4
     full = SofaIndex(x, sample_size=3000)
     d0, i0 = full.knn(q, k)
     model = full.raw_model
-    ds, is_ = [], []
+    xn, qn = x.cpu().numpy(), q.cpu().numpy()
+    ds, is_, ods, ois = [], [], [], []
     for r in range(parts):
         a, b = datagen.shard_range(w.n_series, r, parts)
         sh = x[a:b].contiguous()
@@ -174,9 +155,56 @@ def test_sharded_merge_equals_unsharded(parts):
         d, i = ix.knn(q, k)
         ds.append(d)
         is_.append(i)
+        do_, io_ = O.knn_bruteforce(xn[a:b], qn, k)
+        assert_knn_parity(d.cpu().numpy(), i.cpu().numpy() - a, do_, io_, xn[a:b], qn)  # each shard is exact
+        ods.append(do_)
+        ois.append(np.where(io_ >= 0, io_ + a, -1))
         del ix
     md, mi = merge_topk(torch.stack(ds), torch.stack(is_))
     assert torch.equal(mi, i0) and torch.equal(md, d0)
+    od, oi = O.merge_topk(np.stack(ods), np.stack(ois), k)
+    assert_knn_parity(md.cpu().numpy(), mi.cpu().numpy(), od, oi, xn, qn)
+    do, io = O.knn_bruteforce(xn, qn, k)
+    assert_knn_parity(md.cpu().numpy(), mi.cpu().numpy(), do, io, xn, qn)
+
+
+@pytest.mark.parametrize("P,Q,k", [(2, 50, 1), (3, 17, 5), (8, 9, 16), (5, 4, 128)])
+def test_merge_kernel_equals_oracle_merge(P, Q, k):
+    """k_merge_topk alone on synthetic sorted lists with exact ties (across and within parts),
+    padding and empty parts: equal to O.merge_topk element by element (ties -> smaller index)"""
+    rng = np.random.default_rng(P * 100 + k)
+    d = np.sort(rng.integers(0, 6, size=(P, Q, k)).astype(np.float32) * 0.25, axis=2)
+    i = np.empty((P, Q, k), dtype=np.int64)
+    for p in range(P):
+        for qq in range(Q):  # distinct global indices per part, increasing within equal distances
+            i[p, qq] = np.sort(rng.choice(10 ** 6, size=k, replace=False)) * P + p
+    pad = rng.random((P, Q, k)) < 0.2
+    pad = np.cumsum(pad, axis=2) > 0          # padding is a suffix of each list
+    d[pad] = np.inf
+    i[pad] = -1
+    d[0, 0] = np.inf                          # an empty part
+    i[0, 0] = -1
+    md, mi = merge_topk(torch.from_numpy(d).cuda(), torch.from_numpy(i).cuda())
+    od, oi = O.merge_topk(d.astype(np.float64), i, k)
+    assert np.array_equal(mi.cpu().numpy(), oi)
+    assert np.array_equal(md.cpu().numpy().astype(np.float64), od)
+
+
+@pytest.mark.parametrize("k", [1, 5])
+def test_large_leaf_list_branch_parity(k):
+    """the front's large-list branch (more than CAP_B = 2048 leaves survive the envelope filter and
+    the top-M re-filter: the ~1536 lowest-LB leaves are sorted and scanned first, the rest is
+    re-filtered and scanned in storage order): 1M rows in blocks of 32 (31,250 leaves), noisy
+    members with sigma = 1 (SFA bound weak: most leaves survive), sparse path forced"""
+    w = datagen.scaled(datagen.WORKLOADS["cfg4"], 1_000_000, 12, noise_sigmas=(1.0,))
+    x, q = _data(w)
+    ix = SofaIndex(x, sample_size=10_000, block_size=32, dense_permille=-1)
+    d, i, st = ix.knn(q, k, stats=True)
+    torch.cuda.synchronize()
+    assert st["rounds"] > 0 and st["max_list_blocks"] > 2048, st  # the cnt > CAP_B branch ran
+    xn, qn = x.cpu().numpy(), q.cpu().numpy()
+    do, io = O.knn_bruteforce(xn, qn, k)
+    assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, xn, qn)
 
 
 def test_bsf_init_prunes_without_changing_results():
@@ -248,32 +276,6 @@ def test_host_path_equals_device_path():
     assert np.array_equal(hi, i.cpu().numpy()) and np.array_equal(hd, d.cpu().numpy())
 
 
-@pytest.mark.slow
-def test_cfg2_full_size_sampled():
-    """BJ configs[1] at full size (10M x 256, 1000 noisy queries) in the bench's launch
-    configuration: every query's 1-NN is its source member (known answer for sigma=0.1,
-    SURVEY 8(c)), and 3 sampled queries match the oracle's brute force over all 10M rows."""
-    w = datagen.WORKLOADS["cfg2"]
-    x = datagen.generate_rows(w, 0, w.n_series, device="cuda")
-    q = datagen.generate_queries(w, device="cuda", data=x)
-    ix = SofaIndex(x, sample_size=datagen.default_sample_size(w))
-    d, i = ix.knn(q, 1)
-    src = datagen.query_sources(w)
-    assert np.array_equal(i[:, 0].cpu().numpy(), src)
-    pick = [0, 499, 998]
-    qn = q[pick].cpu().numpy()
-    best_d = np.full(3, np.inf)
-    best_i = np.full(3, -1)
-    for s in range(0, w.n_series, 1 << 20):
-        chunk = x[s:s + (1 << 20)].cpu().numpy()
-        dd, ii = O.knn_bruteforce(chunk, qn, 1)
-        better = dd[:, 0] < best_d
-        best_d[better] = dd[better, 0]
-        best_i[better] = ii[better, 0] + s
-    np.testing.assert_allclose(d[pick, 0].cpu().numpy(), best_d, rtol=DIST_RTOL)
-    assert np.array_equal(i[pick, 0].cpu().numpy(), best_i)
-
-
 @pytest.mark.parametrize("Q,k", [(3, 1), (7, 4), (40, 2)])
 def test_scan_pool_heavy_queries(Q, k):
     """few queries with long leaf lists (cfg4 recipe, sigma 1.0 members) on the sparse path: their
@@ -343,40 +345,42 @@ def test_knn_seed_bound_is_a_valid_upper_bound(kind, k):
     assert torch.equal(i1, i2) and torch.equal(d1, d2)
 
 
-@pytest.mark.parametrize("rev_rounds", ["0", "1", "1000000"])
-@pytest.mark.parametrize("kind,k,front_batches", [("cfg1", 5, "16"), ("cfg4", 3, "2")])
-def test_revisit_pass_and_front_split(monkeypatch, rev_rounds, kind, k, front_batches):
+@pytest.mark.parametrize("rev_rounds", [0, 1, 1000000])
+@pytest.mark.parametrize("kind,k,front_batches", [("cfg1", 5, 16), ("cfg4", 3, 2)])
+def test_revisit_pass_and_front_split(rev_rounds, kind, k, front_batches):
     """scan_blocks' revisit pass (a leaf part with more than rev_rounds x R candidates is deferred
     until after the list; 0 defers every part with a candidate and overflows the revisit queue,
     1e6 never defers) and the front/scan split (front_batches word batches in the front, the rest
     as scan tasks) change the refinement order only: results equal the oracle's brute force and
-    each other bit for bit (tuning knobs read by the library at every launch)"""
-    monkeypatch.setenv("SOFA_REV_ROUNDS", rev_rounds)
-    monkeypatch.setenv("SOFA_FRONT_BATCHES", front_batches)
+    each other bit for bit (sofa_set_tuning)"""
     w = datagen.scaled(datagen.WORKLOADS[kind], 200_000 + 33, 24)
     x, q = _data(w)
     ix = SofaIndex(x, sample_size=3000, dense_permille=-1)
+    ix.set_tuning(rev_rounds=rev_rounds, front_batches=front_batches)
     d, i, st = ix.knn(q, k, stats=True)
     torch.cuda.synchronize()
     do, io = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), k)
     assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, x.cpu().numpy(), q.cpu().numpy())
-    monkeypatch.setenv("SOFA_REV_ROUNDS", "1000000")
-    monkeypatch.setenv("SOFA_FRONT_BATCHES", "1000000")
+    ix.set_tuning(rev_rounds=1000000, front_batches=1000000)
     d2, i2 = ix.knn(q, k)
     assert torch.equal(d, d2) and torch.equal(i, i2)
 
 
-@pytest.mark.parametrize("kind,k", [("cfg1", 1), ("cfg4", 5)])
-def test_wide_and_narrow_query_builds_agree(monkeypatch, kind, k):
-    """a batch of at most one query per SM runs the 16-warp build of the query kernels (query512.cu);
-    forcing the 8-warp build (SOFA_FRONT_WIDE=0, SOFA_SCAN_WIDE=0) must give the same bits, and both
-    equal the oracle's brute force"""
-    w = datagen.scaled(datagen.WORKLOADS[kind], 150_000 + 7, 37)
+@pytest.mark.parametrize("front_wide,scan_wide", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("kind,k,Q", [("cfg1", 1, 37), ("cfg4", 5, 37), ("cfg4", 2, 400)])
+def test_wide_and_narrow_query_builds_agree(front_wide, scan_wide, kind, k, Q):
+    """the 16-warp (query512.cu) and 8-warp builds of the front and the scan pool, in every pairing —
+    they share QState, the leaf pool and the tasks — give the same bits as the automatic choice and
+    equal the oracle's brute force; the scan pool must actually run (scan tasks published).  Q = 400
+    is more queries than SMs, so 'wide' there forces the 16-warp build past its automatic range."""
+    kw = {"noise_sigmas": (1.0,)} if kind == "cfg4" else {}
+    w = datagen.scaled(datagen.WORKLOADS[kind], 150_000 + 7, Q, **kw)
     x, q = _data(w)
     ix = SofaIndex(x, sample_size=3000, dense_permille=-1)
-    d, i = ix.knn(q, k)
-    monkeypatch.setenv("SOFA_FRONT_WIDE", "0")
-    monkeypatch.setenv("SOFA_SCAN_WIDE", "0")
+    ix.set_tuning(front_batches=1)  # publish most leaves as scan tasks so the scan pool has work
+    d, i, st = ix.knn(q, k, stats=True)
+    assert st["scan_tasks"] > 0
+    ix.set_tuning(front_batches=1, front_wide=front_wide, scan_wide=scan_wide)
     d2, i2 = ix.knn(q, k)
     torch.cuda.synchronize()
     assert torch.equal(d, d2) and torch.equal(i, i2)

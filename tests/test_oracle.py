@@ -254,6 +254,47 @@ def test_bruteforce_query_in_corpus_duplicates_and_padding():
     assert list(i[0, 3:]) == [-1, -1] and np.all(np.isinf(d[0, 3:]))
 
 
+def _chunks(data, sizes):
+    s = 0
+    for c in sizes:
+        yield s, data[s:s + c]
+        s += c
+
+
+@pytest.mark.parametrize("N,n,k,sizes,gemm", [(1, 4, 1, [1], 8), (7, 16, 3, [2, 5], 3), (100, 16, 5, [33, 0, 67], 16),
+                                              (300, 32, 300, [100, 100, 100], 64), (257, 8, 4, [1, 255, 1], 7)])
+def test_stream_bruteforce_equals_python_loops(N, n, k, sizes, gemm):
+    """the streamed brute force (chunked rows, float64 GEMM shortlist + exact direct sums) against
+    the pure-Python definition, including empty chunks, k = N and k above a chunk's size"""
+    rng = np.random.default_rng(N * n + k)
+    data = rng.normal(size=(N, n)).astype(np.float32)
+    qs = rng.normal(size=(3, n)).astype(np.float32)
+    d, i = O.knn_bruteforce_stream(_chunks(data, sizes), qs, k, rows_per_gemm=gemm)
+    for r in range(3):
+        pd, pi = _py_knn(data.astype(np.float64), qs[r].astype(np.float64), k)
+        np.testing.assert_allclose(d[r, :len(pd)], pd, rtol=1e-12)
+        assert list(i[r, :len(pi)]) == pi
+
+
+def test_stream_bruteforce_ties_across_chunks_and_padding():
+    """exact duplicates in different chunks -> smaller index first; a constant row -> zero vector;
+    k above N pads with (+inf, -1); agrees with knn_bruteforce on a random-walk set"""
+    rng = np.random.default_rng(12)
+    data = np.cumsum(rng.normal(size=(500, 64)), axis=1).astype(np.float32)
+    data[420] = data[17]
+    data[421] = 5.0
+    qs = np.concatenate([data[[17, 421]], np.cumsum(rng.normal(size=(4, 64)), axis=1).astype(np.float32)])
+    d, i = O.knn_bruteforce_stream(_chunks(data, [100, 300, 100]), qs, 3, rows_per_gemm=64)
+    assert list(i[0, :2]) == [17, 420] and d[0, 0] == 0 and d[0, 1] == 0
+    assert i[1, 0] == 421 and d[1, 0] == 0   # constant query vs constant row: both zero vectors
+    d2, i2 = O.knn_bruteforce(data, qs, 3)
+    np.testing.assert_allclose(d, d2, rtol=1e-12)
+    keep = [0, 2, 3, 4, 5]   # (the constant query ties every row at d^2 = n up to float64 rounding)
+    assert np.array_equal(i[keep], i2[keep])
+    d3, i3 = O.knn_bruteforce_stream(_chunks(data[:2], [2]), qs[:1], 4)
+    assert list(i3[0, 2:]) == [-1, -1] and np.all(np.isinf(d3[0, 2:]))
+
+
 @pytest.mark.parametrize("n,l,a,k", [(16, 4, 4, 1), (32, 8, 16, 3), (64, 16, 256, 1), (64, 16, 256, 10)])
 def test_gemini_equals_bruteforce(n, l, a, k):
     x = _rw(1200, n, n + l)
