@@ -1,5 +1,6 @@
 // Shared device helpers and the internal index layout of libsofa (sm_100a).
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -77,31 +78,45 @@ __device__ __forceinline__ float warp_sum_f32(float v) {
   return v;
 }
 
-// a1 (Def. 2, population std, reading 1): per-row statistics computed by ONE warp with
-// a fixed arithmetic order, shared by the series transform and the query prep so that a query
-// equal to a stored row z-normalises to the same float32 bits (exact duplicates -> d = 0).
-// Each lane sums its float4s (lane + 32 f) in float32, the 32 partials are combined in float64.
-// Returns mu (float32), inv_sigma (float64; 0 for a constant row), and the float64 mu.
-template <int NF>
-__device__ __forceinline__ void row_stats(const float4 (&x)[NF], int nf4, int len, float& muf, double& mu64,
-                                          double& inv64) {
-  const int lane = threadIdx.x & 31;
+// Lanes per row in the row layout of a1 (k_transform and the query prep): each lane of a group of G
+// lanes holds 8 float4 of the row (float4 index g + G f), G = ceil(n/32) rounded up to a power of two.
+__host__ __device__ constexpr int row_group(int nf4) {
+  int G = 1;
+  while (G * 8 < nf4) G *= 2;
+  return G;
+}
+
+// a1 (Def. 2, population std, reading 1): per-row statistics with a fixed arithmetic order,
+// shared by the series transform and the query prep so that a query equal to a stored row
+// z-normalises to the same float32 bits (exact duplicates -> d = 0).  Each lane of the row's group
+// sums its float4s in float32, the G partials are combined in float64 by an xor butterfly (every
+// lane of the group ends with the same value).  Returns mu (float32 and float64) and inv_sigma
+// (float64; 0 for a constant row).
+template <int G>
+__device__ __forceinline__ void row_stats_g(const float4 (&x)[8], int nf4, int g, int len, float& muf, double& mu64,
+                                            double& inv64) {
   float p = 0.f;
 #pragma unroll
-  for (int f = 0; f < NF; ++f)
-    if (lane + 32 * f < nf4) p = __fadd_rn(p, __fadd_rn(__fadd_rn(x[f].x, x[f].y), __fadd_rn(x[f].z, x[f].w)));
-  mu64 = warp_sum_f64((double)p) / (double)len;
+  for (int f = 0; f < 8; ++f)
+    if (g + G * f < nf4) p = __fadd_rn(p, __fadd_rn(__fadd_rn(x[f].x, x[f].y), __fadd_rn(x[f].z, x[f].w)));
+  double sp = (double)p;
+#pragma unroll
+  for (int m = G / 2; m >= 1; m >>= 1) sp += __shfl_xor_sync(FULL, sp, m);
+  mu64 = sp / (double)len;
   muf = (float)mu64;
   float s = 0.f;
 #pragma unroll
-  for (int f = 0; f < NF; ++f)
-    if (lane + 32 * f < nf4) {
-      float a = __fsub_rn(x[f].x, muf), b = __fsub_rn(x[f].y, muf);
-      float c = __fsub_rn(x[f].z, muf), d = __fsub_rn(x[f].w, muf);
+  for (int f = 0; f < 8; ++f)
+    if (g + G * f < nf4) {
+      const float a = __fsub_rn(x[f].x, muf), b = __fsub_rn(x[f].y, muf);
+      const float c = __fsub_rn(x[f].z, muf), d = __fsub_rn(x[f].w, muf);
       s = __fadd_rn(s, __fadd_rn(__fmaf_rn(a, a, __fmul_rn(b, b)), __fmaf_rn(c, c, __fmul_rn(d, d))));
     }
-  double var = warp_sum_f64((double)s) / (double)len;
-  double sd = sqrt(var);
+  double ss = (double)s;
+#pragma unroll
+  for (int m = G / 2; m >= 1; m >>= 1) ss += __shfl_xor_sync(FULL, ss, m);
+  const double var = ss / (double)len;
+  const double sd = sqrt(var);
   inv64 = sd < 1e-12 ? 0.0 : 1.0 / sd;
 }
 
@@ -307,8 +322,9 @@ struct sofa_index {
 
 namespace sofa {
 int upload_model(const sofa_model& m, int len, sofa_index* ix, cudaStream_t st);
-int launch_transform(const float* X, int64_t N, const DevModel& dm, uint8_t* words, float2* stats, uint64_t* keys,
-                     double* vals, uint8_t* words_l, cudaStream_t st);
+int launch_transform(const float* X, int64_t N, const DevModel& dm, const sofa_model& m, uint8_t* words,
+                     float2* stats, uint64_t* keys, double* vals, uint8_t* words_l, __nv_bfloat16* xb16,
+                     cudaStream_t st);
 int launch_envelopes(const uint8_t* words, int64_t n, int B, int WS, const uint64_t* skeys, uint8_t* env,
                      uint64_t* bkey, cudaStream_t st);
 int launch_env_up(const uint8_t* child, int64_t nchild, int WS, uint8_t* parent, cudaStream_t st);

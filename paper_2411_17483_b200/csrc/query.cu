@@ -832,21 +832,31 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
     t_phase[0] = clock64();
     // ---------------------------------------------------------------- a5: z-norm + projection
     if (warp == 0) {
+      // the row layout and statistics of k_transform (row_stats_g): every group of G lanes holds the
+      // whole query, group 0 writes q-hat
       const float4* q4 = reinterpret_cast<const float4*>(A.Q + (int64_t)qi * len);
-      float4 x[NF];
+      const int G = row_group(nf4), g = lane & (G - 1);
+      float4 x[8];
 #pragma unroll
-      for (int f = 0; f < NF; ++f) {
-        const int fi = lane + 32 * f;
+      for (int f = 0; f < 8; ++f) {
+        const int fi = g + G * f;
         x[f] = fi < nf4 ? q4[fi] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
       float muf;
       double mu64, inv64;
-      row_stats<NF>(x, nf4, len, muf, mu64, inv64);
+      switch (G) {
+        case 1: row_stats_g<1>(x, nf4, g, len, muf, mu64, inv64); break;
+        case 2: row_stats_g<2>(x, nf4, g, len, muf, mu64, inv64); break;
+        case 4: row_stats_g<4>(x, nf4, g, len, muf, mu64, inv64); break;
+        case 8: row_stats_g<8>(x, nf4, g, len, muf, mu64, inv64); break;
+        case 16: row_stats_g<16>(x, nf4, g, len, muf, mu64, inv64); break;
+        default: row_stats_g<32>(x, nf4, g, len, muf, mu64, inv64); break;
+      }
       const float invf = (float)inv64;
 #pragma unroll
-      for (int f = 0; f < NF; ++f) {
-        const int fi = lane + 32 * f;
-        if (fi < nf4) {
+      for (int f = 0; f < 8; ++f) {
+        const int fi = lane + G * f;
+        if (lane < G && fi < nf4) {
           float4 h;
           h.x = __fmul_rn(__fsub_rn(x[f].x, muf), invf);
           h.y = __fmul_rn(__fsub_rn(x[f].y, muf), invf);

@@ -365,7 +365,7 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
   const int64_t env_nodes = ix->lvl_off[ix->nlev - 1] + ix->lvl_cnt[ix->nlev - 1];
   BCK(cudaMalloc(&ix->env, (size_t)env_nodes * 2 * WS));
   BCK(cudaMalloc(&ix->bkey, (size_t)ix->nb * 8));
-  if ((rc = launch_transform(series_dev, n, ix->dm, words_u, stats_u, keys_u, nullptr, nullptr, st))) {
+  if ((rc = launch_transform(series_dev, n, ix->dm, ix->model, words_u, stats_u, keys_u, nullptr, nullptr, nullptr, st))) {
     freeall();
     return bail(rc);
   }
@@ -605,7 +605,7 @@ int sofa_transform(const float* series_dev, int64_t n, const sofa_model* model, 
   sofa_index tmp;
   cudaStream_t st = (cudaStream_t)cuda_stream;
   rc = upload_model(*model, model->len, &tmp, st);
-  if (!rc) rc = launch_transform(series_dev, n, tmp.dm, nullptr, nullptr, nullptr, out_values_dev, out_words_dev, st);
+  if (!rc) rc = launch_transform(series_dev, n, tmp.dm, *model, nullptr, nullptr, nullptr, out_values_dev, out_words_dev, nullptr, st);
   cudaStreamSynchronize(st);
   void* ps[] = {tmp.basis32, tmp.basis64, tmp.edges32, tmp.edges64};
   for (void* p : ps)

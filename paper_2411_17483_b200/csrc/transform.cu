@@ -1,196 +1,375 @@
 // a1 + a3 (z-norm statistics, SFA projection, quantisation) and a4 (block layout helpers).
 //
-// k_transform is one HBM pass over the series (Alg. 2, applied to every row):
-//   * one warp owns SER consecutive rows; lane holds float4 columns lane + 32 f (coalesced
-//     512 B per warp-load, L1::no_allocate streaming);
-//   * mean / std per row with the shared row_stats() (float32 lane partials, float64 combine);
-//   * projection onto the LT selected basis rows (cos / -sin(2 pi k t/n) / sqrt(n), staged in
-//     shared memory as float4 so a warp-load of the basis is 512 contiguous bytes): every lane
-//     accumulates 4*NF-term float32 partial dot products, then a reduce-scatter butterfly over the
-//     32 lanes leaves each lane with fully reduced (row, coefficient) values;
-//   * value * (1/sigma) in float64, symbol = upper_bound over the float32 edge row (bins
-//     [beta(s), beta(s+1))), key for a4, write word / stats / key.
-// The projection is a dense [rows x n] x [n x l] contraction at 8 flop/B (n=256,l=16): FP32 FFMA
-// keeps it at the HBM roofline on B200; the accuracy budget (symbols bit-exact outside 1e-5 of an
-// edge, SURVEY 8(c) reading 24) rules out 1xTF32.  See DESIGN.md "K2".
+// k_transform is one HBM pass over the series (Alg. 2, applied to every row).
+// Layout: a row is owned by a GROUP of G lanes (G = n/32 rounded up to a power of two, so each lane
+// holds 8 float4 = 32 values: float4 index g + G*f, f < 8); a warp holds 32/G rows at once.  The
+// group layout keeps the cross-lane work per row small (log2 G butterfly stages instead of 5).
+//   * row statistics with row_stats_g (common.cuh; the query prep uses the same function, so a
+//     query equal to a stored row z-normalises to the same float32 bits);
+//   * DFT symmetry fold (n = 32 G, a DFT model): a selected position is Re X_k (basis cos, even
+//     about t = 0 mod n) or Im X_k (basis -sin, odd), so with u_t = x_t + x_{n-t} and
+//     v_t = x_t - x_{n-t} the dot products need only t < n/2: Re rows use u (the t = n/2 term
+//     folded into u_0 as x_0 +- x_{n/2}, the sign being cos(pi k)), Im rows use v.  The partner
+//     x_{n-t} of the value a lane holds sits in lane G-1-g (or G-g for the first component) of the
+//     same group at slot 7-f: 4 sub-group shuffles per slot pair.  This halves the FFMA work; the
+//     basis rows are processed in the order [Re even k | Re odd k | Im] (a permutation of the
+//     model's positions, undone when the symbols are written);
+//   * float32 FFMA partial dot products, then a reduce-scatter butterfly over the group leaves
+//     each lane with fully reduced (row, coefficient) values;
+//   * value * (1/sigma), symbol = number of float32 edges <= value (binary search over the edge row
+//     in shared memory; float32 rounding moves a value by ~1e-7 relative, inside reading 24's
+//     1e-5 edge exemption), the a4 key bits of the lane's symbols OR-reduced over the group;
+//   * optionally the z-normalised row as bfloat16 (original row order) for the dense screen (f1).
+// Work per n = 256 row: 64 warp-FFMA (folded) + ~120 other instructions, i.e. ~45 SM cycles, below
+// the ~43-cycle HBM budget of one 1 KB row per SM only with good overlap — the kernel is designed to
+// be HBM-bound, not measured to be here (see profiles/).  The accuracy budget (symbols bit-exact
+// outside 1e-5 of an edge, SURVEY 8(c) reading 24) rules out 1xTF32 tensor cores.
 #include <cub/cub.cuh>
+
+#include <cuda_bf16.h>
 
 #include "common.cuh"
 
 namespace sofa {
 
-template <int V, int M = 16>
-__device__ __forceinline__ void reduce_scatter(float* v, int lane) {
+// Reduce-scatter over the G lanes of a group: V values per lane in, after log2(G) stages lane g of
+// the group holds the group-sum of value g*(V/G)+i in v[i] (V >= G) or, if V < G, every lane holds
+// the sum of value g/(G/V) in v[0].
+template <int V, int M>
+__device__ __forceinline__ void reduce_scatter_g(float* v, int lane) {
   if constexpr (M >= 1) {
     if constexpr (V > 1) {
       constexpr int H = V / 2;
       const bool up = (lane & M) != 0;
 #pragma unroll
       for (int i = 0; i < H; ++i) {
-        float send = up ? v[i] : v[i + H];
-        float keep = up ? v[i + H] : v[i];
+        const float send = up ? v[i] : v[i + H];
+        const float keep = up ? v[i + H] : v[i];
         v[i] = keep + __shfl_xor_sync(FULL, send, M);
       }
-      reduce_scatter<H, M / 2>(v, lane);
+      reduce_scatter_g<H, M / 2>(v, lane);
     } else {
       v[0] += __shfl_xor_sync(FULL, v[0], M);
-      reduce_scatter<1, M / 2>(v, lane);
+      reduce_scatter_g<1, M / 2>(v, lane);
     }
   }
 }
 
-template <int NF, int LT, int SER>
-__global__ void __launch_bounds__(kThreads, 2)
-    k_transform(const float* __restrict__ X, int64_t N, int len, int l, int a_bits, int WS,
-                const float* __restrict__ basis32, const float* __restrict__ edges32, uint8_t* __restrict__ words,
-                float2* __restrict__ stats, uint64_t* __restrict__ keys, double* __restrict__ vals,
-                uint8_t* __restrict__ words_l, int basis_in_smem) {
+struct TransformArgs {
+  const float* X;
+  int64_t N;
+  int len, l, a_bits, WS;
+  int n_re_even, n_re_odd;      // fold: basis rows [0, ne) Re with even k, [ne, ne+no) Re odd k, rest Im
+  const float* basis;           // LT x (8 G) float4-slots: folded (4 slots) or full (8 slots) layout
+  const int* order;             // LT: processing row jj -> model position j
+  const float* edges32;
+  uint8_t* words;
+  float2* stats;
+  uint64_t* keys;
+  double* vals;
+  uint8_t* words_l;
+  __nv_bfloat16* xb16;          // nullable: N x len z-normalised rows (dense screen operand)
+};
+
+// 2 CTAs (16 warps, up to 128 registers) when the fold or wide words need the registers, else 3
+template <int G, int LT, bool FOLD>
+__global__ void __launch_bounds__(kThreads, (FOLD || LT > 16) ? 2 : 3) k_transform(const __grid_constant__ TransformArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int nf4 = len >> 2;
-  // basis rows in shared memory when they fit (LT*len*4 bytes), else read through L1/L2
-  const size_t basis_bytes = basis_in_smem ? (size_t)LT * len * 4 : 0;
-  float4* s_basis = reinterpret_cast<float4*>(smem);                      // LT x nf4
-  float* s_edges = reinterpret_cast<float*>(smem + basis_bytes);          // LT x 256
-  uint8_t* s_w = reinterpret_cast<uint8_t*>(s_edges + LT * 256);         // 8 x SER x LT
+  constexpr int RPW = 32 / G;                 // rows per warp
+  constexpr int NS = FOLD ? 4 : 8;            // basis slots per lane
+  constexpr int VPL = LT >= G ? LT / G : 1;   // reduced values per lane
+  constexpr int OWN = LT >= G ? 1 : G / LT;   // lanes sharing one value when LT < G
+  const int len = A.len, nf4 = len >> 2, l = A.l;
+  float4* s_basis = reinterpret_cast<float4*>(smem);                           // LT x NS x G
+  float* s_edges = reinterpret_cast<float*>(smem + (size_t)LT * NS * G * 16);  // LT x 256 (model order)
+  uint8_t* s_w = reinterpret_cast<uint8_t*>(s_edges + LT * 256);               // 8 warps x RPW x LT
+  int* s_ord = reinterpret_cast<int*>(s_w + 8 * RPW * LT);                      // LT
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (basis_in_smem)
-    for (int i = tid; i < LT * nf4; i += kThreads) s_basis[i] = reinterpret_cast<const float4*>(basis32)[i];
-  const float4* bas = basis_in_smem ? s_basis : reinterpret_cast<const float4*>(basis32);
-  for (int i = tid; i < LT * 256; i += kThreads) s_edges[i] = edges32[i];
-  for (int i = tid; i < 8 * SER * LT; i += kThreads) s_w[i] = 0;
+  const int g = lane & (G - 1), rw = lane / G;  // lane in group, row of the warp
+  for (int i = tid; i < LT * NS * G; i += kThreads) s_basis[i] = reinterpret_cast<const float4*>(A.basis)[i];
+  for (int i = tid; i < LT * 256; i += kThreads) s_edges[i] = A.edges32[i];
+  for (int i = tid; i < 8 * RPW * LT; i += kThreads) s_w[i] = 0;
+  for (int i = tid; i < LT; i += kThreads) s_ord[i] = A.order[i];
   __syncthreads();
-  uint8_t* my_w = s_w + warp * SER * LT;
+  uint8_t* my_w = s_w + warp * RPW * LT;
+  const int ne = A.n_re_even, nre = A.n_re_even + A.n_re_odd;
+  const float c0x2 = (float)(2.0 / sqrt((double)A.len));  // 2 C(0) = 2 / sqrt(n)
+  const int P = l < 16 ? l : 16;  // key positions
+  const int sh8 = 8 - A.a_bits;
 
-  constexpr int V = SER * LT;
-  constexpr int VPL = V >= 32 ? V / 32 : 1;
-  constexpr int G = V >= 32 ? 1 : 32 / V;
-
-  for (int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * SER; r0 < N; r0 += (int64_t)gridDim.x * 8 * SER) {
-    float4 x[SER][NF];
+  for (int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * RPW; r0 < A.N; r0 += (int64_t)gridDim.x * 8 * RPW) {
+    const int64_t row = r0 + rw;
+    const bool live = row < A.N;
+    const float4* xr = reinterpret_cast<const float4*>(A.X + row * len);
+    float4 x[8];
 #pragma unroll
-    for (int s = 0; s < SER; ++s) {
-      const int64_t row = r0 + s;
+    for (int f = 0; f < 8; ++f) {
+      const int fi = g + G * f;
+      x[f] = (live && fi < nf4) ? ld_stream(xr + fi) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float muf;
+    double mu64, inv64;
+    row_stats_g<G>(x, nf4, g, len, muf, mu64, inv64);
 #pragma unroll
-      for (int f = 0; f < NF; ++f) {
-        const int fi = lane + 32 * f;
-        x[s][f] = (row < N && fi < nf4) ? ld_stream(reinterpret_cast<const float4*>(X + row * len) + fi)
-                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int f = 0; f < 8; ++f) {
+      x[f].x = __fsub_rn(x[f].x, muf);
+      x[f].y = __fsub_rn(x[f].y, muf);
+      x[f].z = __fsub_rn(x[f].z, muf);
+      x[f].w = __fsub_rn(x[f].w, muf);
+    }
+    if (A.xb16 && live) {  // z-normalised row in bfloat16 (round to nearest), original order
+      const float invf = (float)inv64;
+#pragma unroll
+      for (int f = 0; f < 8; ++f) {
+        const int fi = g + G * f;
+        if (fi < nf4) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(x[f].x * invf, x[f].y * invf);
+          __nv_bfloat162 hi = __floats2bfloat162_rn(x[f].z * invf, x[f].w * invf);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(A.xb16 + row * len + 4 * fi) = pk;
+        }
       }
     }
-    float muf[SER];
-    double inv[SER];
+    float acc[LT];
 #pragma unroll
-    for (int s = 0; s < SER; ++s) {
-      double mu64;
-      row_stats<NF>(x[s], nf4, len, muf[s], mu64, inv[s]);
+    for (int j = 0; j < LT; ++j) acc[j] = 0.f;
+    float nyq_row = 0.f;  // fold: x_{n/2} - mu of this lane's row
+    if constexpr (FOLD) {
+      // u into x[f], v into x[7-f] (f < 4); pairs processed from the middle out so lane 0's
+      // first-component partners x[8-f].x are read before their slot is overwritten
+      const float nyq = x[4].x;  // lane g = 0: x_{n/2}
+      const float x0 = x[0].x;   // lane g = 0: x_0 (no partner)
 #pragma unroll
-      for (int f = 0; f < NF; ++f) {
-        x[s][f].x = __fsub_rn(x[s][f].x, muf[s]);
-        x[s][f].y = __fsub_rn(x[s][f].y, muf[s]);
-        x[s][f].z = __fsub_rn(x[s][f].z, muf[s]);
-        x[s][f].w = __fsub_rn(x[s][f].w, muf[s]);
+      for (int f = 3; f >= 0; --f) {
+        const int src1 = G - 1 - g, src0 = (G - g) & (G - 1);
+        const float p1 = __shfl_sync(FULL, x[7 - f].w, (lane & ~(G - 1)) | src1);
+        const float p2 = __shfl_sync(FULL, x[7 - f].z, (lane & ~(G - 1)) | src1);
+        const float p3 = __shfl_sync(FULL, x[7 - f].y, (lane & ~(G - 1)) | src1);
+        float p0 = __shfl_sync(FULL, x[7 - f].x, (lane & ~(G - 1)) | src0);
+        if (g == 0) p0 = f > 0 ? x[8 - f].x : 0.f;  // lane 0: partner in its own slot 8-f; t = 0 has none
+        const float4 a = x[f];
+        x[f] = make_float4(__fadd_rn(a.x, p0), __fadd_rn(a.y, p1), __fadd_rn(a.z, p2), __fadd_rn(a.w, p3));
+        x[7 - f] = make_float4(__fsub_rn(a.x, p0), __fsub_rn(a.y, p1), __fsub_rn(a.z, p2), __fsub_rn(a.w, p3));
+      }
+      if (g == 0) x[0].x = __fadd_rn(x0, nyq);  // u_0 = x_0 + x_{n/2}: exact for Re rows with even k
+      // processing rows [Re | Im]: u (x[0..3]) for the Re rows, then the registers are swapped once so
+      // that x[0..3] hold v for the Im rows (one uniform check per row instead of a select per value)
+      const float4* bs = s_basis + g;
+#pragma unroll
+      for (int j = 0; j < LT; ++j) {
+        if (j == nre) {
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            const float4 t = x[f];
+            x[f] = x[7 - f];
+            x[7 - f] = t;
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          const float4 b = bs[(j * 4 + f) * G];
+          float s = acc[j];
+          s = fmaf(x[f].x, b.x, s);
+          s = fmaf(x[f].y, b.y, s);
+          s = fmaf(x[f].z, b.z, s);
+          s = fmaf(x[f].w, b.w, s);
+          acc[j] = s;
+        }
+      }
+      nyq_row = __shfl_sync(FULL, nyq, lane & ~(G - 1));
+    } else {
+      const float4* bs = s_basis + g;
+#pragma unroll
+      for (int j = 0; j < LT; ++j) {
+        if (j >= l) break;
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+          const float4 b = bs[(j * 8 + f) * G];
+          float s = acc[j];
+          s = fmaf(x[f].x, b.x, s);
+          s = fmaf(x[f].y, b.y, s);
+          s = fmaf(x[f].z, b.z, s);
+          s = fmaf(x[f].w, b.w, s);
+          acc[j] = s;
+        }
       }
     }
-    float acc[V];
+    reduce_scatter_g<LT, G / 2>(acc, lane);
+    // this lane's reduced values: processing rows jj = g*VPL + i (or g/OWN), model position s_ord[jj]
+    unsigned long long key = 0ull;
+    if (g % OWN == 0) {
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc[i] = 0.f;
+      for (int i = 0; i < VPL; ++i) {
+        const int jj = LT >= G ? g * VPL + i : g / OWN;
+        if (jj < l) {
+          const int j = s_ord[jj];
+          // Re rows with odd k: u_0 held x_0 + x_{n/2}, their t = n/2 term is -x_{n/2} C(0)
+          const float a = FOLD && jj >= ne && jj < nre ? fmaf(-c0x2, nyq_row, acc[i]) : acc[i];
+          const double vd = (double)a * inv64;
+          if (A.vals && live) A.vals[row * l + j] = vd;
+          const float v = (float)vd;
+          const float* e = s_edges + j * 256;
+          int pos = 0;
 #pragma unroll
-    for (int f = 0; f < NF; ++f) {
-      const int fi = lane + 32 * f;
-      if (fi < nf4) {
+          for (int step = 128; step >= 1; step >>= 1)
+            if (e[pos + step - 1] <= v) pos += step;
+          my_w[rw * LT + j] = (uint8_t)pos;
+          if (j < P) {  // a4 key bits of this position: 2-bit digits, MSB first, round-robin
+            const uint32_t s8 = ((uint32_t)pos << sh8) & 0xffu;
 #pragma unroll
-        for (int j = 0; j < LT; ++j) {
-          const float4 b = bas[j * nf4 + fi];
-#pragma unroll
-          for (int s = 0; s < SER; ++s) {
-            float a = acc[s * LT + j];
-            a = fmaf(x[s][f].x, b.x, a);
-            a = fmaf(x[s][f].y, b.y, a);
-            a = fmaf(x[s][f].z, b.z, a);
-            a = fmaf(x[s][f].w, b.w, a);
-            acc[s * LT + j] = a;
+            for (int r = 0; r < 4; ++r) {
+              const int o = r * 2 * P + 2 * j;
+              if (o < 64) key |= (unsigned long long)((s8 >> (6 - 2 * r)) & 3u) << (62 - o);
+            }
           }
         }
       }
     }
-    reduce_scatter<V>(acc, lane);
-    if (lane % G == 0) {
 #pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        const int idx = V >= 32 ? lane * VPL + i : lane / G;
-        const int s = idx / LT, j = idx % LT;
-        const int64_t row = r0 + s;
-        double is = inv[0];
-#pragma unroll
-        for (int t = 1; t < SER; ++t)
-          if (s == t) is = inv[t];
-        if (row < N && j < l) {
-          const double v = (double)acc[i] * is;
-          if (vals) vals[row * l + j] = v;
-          my_w[s * LT + j] = (uint8_t)bin_of(s_edges + j * 256, v);
-        }
-      }
-    }
+    for (int M = G / 2; M >= 1; M >>= 1) key |= __shfl_xor_sync(FULL, key, M);
     __syncwarp();
-#pragma unroll
-    for (int s = 0; s < SER; ++s) {
-      if (lane == s && r0 + s < N) {
-        if (stats) stats[r0 + s] = make_float2(muf[s], (float)inv[s]);
-        if (keys) keys[r0 + s] = word_key(my_w + s * LT, l, a_bits);
-      }
+    if (g == 0 && live) {
+      if (A.stats) A.stats[row] = make_float2(muf, (float)inv64);
+      if (A.keys) A.keys[row] = key;
     }
-    if (words) {
-      const int parts = WS >> 4;
-      for (int c = lane; c < SER * parts; c += 32) {
+    if (A.words) {
+      const int parts = A.WS >> 4;
+      for (int c = lane; c < RPW * parts; c += 32) {
         const int s = c / parts, p = c % parts;
-        if (r0 + s < N)
-          *reinterpret_cast<uint4*>(words + (r0 + s) * WS + p * 16) =
+        if (r0 + s < A.N)
+          *reinterpret_cast<uint4*>(A.words + (r0 + s) * A.WS + p * 16) =
               *reinterpret_cast<const uint4*>(my_w + s * LT + p * 16);
       }
     }
-    if (words_l) {
-      for (int c = lane; c < SER * l; c += 32) {
+    if (A.words_l) {
+      for (int c = lane; c < RPW * l; c += 32) {
         const int s = c / l, j = c % l;
-        if (r0 + s < N) words_l[(r0 + s) * l + j] = my_w[s * LT + j];
+        if (r0 + s < A.N) A.words_l[(r0 + s) * l + j] = my_w[s * LT + j];
       }
     }
     __syncwarp();
   }
 }
 
-template <int NF, int LT>
-static int launch_transform_t(const float* X, int64_t N, const DevModel& dm, uint8_t* words, float2* stats,
-                              uint64_t* keys, double* vals, uint8_t* words_l, cudaStream_t st) {
-  constexpr int SER0 = (4 / NF) < 1 ? 1 : (4 / NF);
-  constexpr int SER = (64 / LT) < SER0 ? (64 / LT) : SER0;
-  auto kern = k_transform<NF, LT, SER>;
-  const size_t basis_bytes = (size_t)LT * dm.len * 4;
-  const int in_smem = basis_bytes <= 96 * 1024;
-  const size_t smem = (in_smem ? basis_bytes : 0) + (size_t)LT * 256 * 4 + 8 * SER * LT;
-  SOFA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t want = (N + 8 * SER - 1) / (8 * SER);
-  int grid = (int)(want < (int64_t)sms * 8 ? want : (int64_t)sms * 8);
-  if (grid < 1) grid = 1;
-  kern<<<grid, kThreads, smem, st>>>(X, N, dm.len, dm.l, dm.a_bits, dm.WS, dm.basis32, dm.edges32, words, stats,
-                                     keys, vals, words_l, in_smem);
-  SOFA_LAUNCHED();
+// Host: the processing order of the basis rows and the per-lane slot layout of the basis.
+// basis32 (DevModel) is LT x len in model order; the kernel wants, per processing row jj and slot
+// (f, g), the float4 of basis values at t = 4 (g + G f) .. +3 (full layout, 8 slots) or the folded
+// values for t < n/2 (4 slots; Re rows: C(t) for t >= 1 and C(0) at t = 0, Im rows: S(t), S(0) = 0).
+int transform_layout(const DevModel& dm, const sofa_model& m, int G, bool fold, std::vector<float>& basis,
+                     std::vector<int>& order, int& ne, int& no) {
+  const int LT = dm.LT, len = dm.len, l = dm.l;
+  const int NS = fold ? 4 : 8;
+  std::vector<int> re_even, re_odd, im;
+  for (int j = 0; j < l; ++j) {
+    const int k = m.best_pos[j] >> 1, isim = m.best_pos[j] & 1;
+    (isim ? im : (k % 2 ? re_odd : re_even)).push_back(j);
+  }
+  order.clear();
+  if (fold) {
+    order.insert(order.end(), re_even.begin(), re_even.end());
+    order.insert(order.end(), re_odd.begin(), re_odd.end());
+    order.insert(order.end(), im.begin(), im.end());
+    ne = (int)re_even.size();
+    no = (int)re_odd.size();
+  } else {
+    for (int j = 0; j < l; ++j) order.push_back(j);
+    ne = l;
+    no = 0;
+  }
+  while ((int)order.size() < LT) order.push_back((int)order.size());
+  // basis values (float64 -> float32) of model position j at time t, computed exactly like k_basis_sel
+  const double rs = 1.0 / std::sqrt((double)len);
+  auto phi = [&](int j, int t) -> double {
+    if (j >= l || t < 0 || t >= len) return 0.0;
+    if (m.binning == SOFA_BINNING_ISAX) {
+      const int seg = len / l;
+      return t / seg == m.best_pos[j] ? 1.0 / seg : 0.0;
+    }
+    const int k = m.best_pos[j] >> 1, isim = m.best_pos[j] & 1;
+    const int mm = (int)(((int64_t)k * t) % len);
+    const double ang = 2.0 * M_PI * mm / len;
+    return isim ? -std::sin(ang) * rs : std::cos(ang) * rs;
+  };
+  basis.assign((size_t)LT * NS * G * 4, 0.f);
+  for (int jj = 0; jj < LT; ++jj) {
+    const int j = jj < l ? order[jj] : l;  // padded rows are zero
+    for (int f = 0; f < NS; ++f)
+      for (int gg = 0; gg < G; ++gg)
+        for (int c = 0; c < 4; ++c) {
+          const int t = 4 * (gg + G * f) + c;
+          basis[(((size_t)jj * NS + f) * G + gg) * 4 + c] = (float)phi(j, t);
+        }
+  }
   return SOFA_OK;
 }
 
-int launch_transform(const float* X, int64_t N, const DevModel& dm, uint8_t* words, float2* stats, uint64_t* keys,
-                     double* vals, uint8_t* words_l, cudaStream_t st) {
+template <int G, int LT, bool FOLD>
+static int launch_transform_t(const TransformArgs& A0, const DevModel& dm, const sofa_model& m, cudaStream_t st) {
+  TransformArgs A = A0;
+  std::vector<float> hb;
+  std::vector<int> ord;
+  int ne = 0, no = 0;
+  transform_layout(dm, m, G, FOLD, hb, ord, ne, no);
+  float* db = nullptr;
+  int* dord = nullptr;
+  SOFA_CK(cudaMallocAsync(reinterpret_cast<void**>(&db), hb.size() * 4, st));
+  SOFA_CK(cudaMallocAsync(reinterpret_cast<void**>(&dord), ord.size() * 4, st));
+  SOFA_CK(cudaMemcpyAsync(db, hb.data(), hb.size() * 4, cudaMemcpyHostToDevice, st));
+  SOFA_CK(cudaMemcpyAsync(dord, ord.data(), ord.size() * 4, cudaMemcpyHostToDevice, st));
+  A.basis = db;
+  A.order = dord;
+  A.n_re_even = ne;
+  A.n_re_odd = no;
+  constexpr int RPW = 32 / G, NS = FOLD ? 4 : 8;
+  auto kern = k_transform<G, LT, FOLD>;
+  const size_t smem = (size_t)LT * NS * G * 16 + (size_t)LT * 256 * 4 + 8 * RPW * LT + LT * 4;
+  SOFA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  SOFA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t want = (A.N + 8 * RPW - 1) / (8 * RPW);
+  int grid = (int)(want < (int64_t)sms * per_sm ? want : (int64_t)sms * per_sm);
+  if (grid < 1) grid = 1;
+  kern<<<grid, kThreads, smem, st>>>(A);
+  SOFA_LAUNCHED();
+  cudaFreeAsync(db, st);
+  cudaFreeAsync(dord, st);
+  return SOFA_OK;
+}
+
+int launch_transform(const float* X, int64_t N, const DevModel& dm, const sofa_model& m, uint8_t* words,
+                     float2* stats, uint64_t* keys, double* vals, uint8_t* words_l, __nv_bfloat16* xb16,
+                     cudaStream_t st) {
   if (N <= 0) return SOFA_OK;
   const int nf4 = dm.len / 4;
-  const int NF = nf4 <= 32 ? 1 : nf4 <= 64 ? 2 : nf4 <= 128 ? 4 : 8;
-#define SOFA_TR(nf, lt) \
-  if (NF == nf && dm.LT == lt) return launch_transform_t<nf, lt>(X, N, dm, words, stats, keys, vals, words_l, st);
-  SOFA_TR(1, 16) SOFA_TR(1, 32) SOFA_TR(1, 64)
-  SOFA_TR(2, 16) SOFA_TR(2, 32) SOFA_TR(2, 64)
-  SOFA_TR(4, 16) SOFA_TR(4, 32) SOFA_TR(4, 64)
-  SOFA_TR(8, 16) SOFA_TR(8, 32) SOFA_TR(8, 64)
+  int G = 1;
+  while (G * 8 < nf4) G *= 2;  // 8 float4 per lane
+  // the fold needs the exact group layout (n = 32 G) and a DFT model (iSAX rows are not symmetric)
+  const bool fold = nf4 == 8 * G && m.binning != SOFA_BINNING_ISAX;
+  TransformArgs A{};
+  A.X = X;
+  A.N = N;
+  A.len = dm.len;
+  A.l = dm.l;
+  A.a_bits = dm.a_bits;
+  A.WS = dm.WS;
+  A.edges32 = dm.edges32;
+  A.words = words;
+  A.stats = stats;
+  A.keys = keys;
+  A.vals = vals;
+  A.words_l = words_l;
+  A.xb16 = xb16;
+#define SOFA_TR(g, lt)                                                                        \
+  if (G == g && dm.LT == lt)                                                                  \
+    return fold ? launch_transform_t<g, lt, true>(A, dm, m, st) : launch_transform_t<g, lt, false>(A, dm, m, st);
+  SOFA_TR(1, 16) SOFA_TR(2, 16) SOFA_TR(4, 16) SOFA_TR(8, 16) SOFA_TR(16, 16) SOFA_TR(32, 16)
+  SOFA_TR(1, 32) SOFA_TR(2, 32) SOFA_TR(4, 32) SOFA_TR(8, 32) SOFA_TR(16, 32) SOFA_TR(32, 32)
+  SOFA_TR(1, 64) SOFA_TR(2, 64) SOFA_TR(4, 64) SOFA_TR(8, 64) SOFA_TR(16, 64) SOFA_TR(32, 64)
 #undef SOFA_TR
   set_error("transform: unsupported (len, l) combination");
   return SOFA_EINVAL;

@@ -7,6 +7,8 @@ from the device to the host in chunks; float64 GEMM shortlist + exact direct sum
 (the source row is the 1-NN) and, on the largest configs, that the index's model equals
 the oracle's model learned from the same strided sample, and the SFA symbols of a strided subset of
 1M rows equal the oracle's outside the edge exemption."""
+import gc
+
 import numpy as np
 import pytest
 import torch
@@ -49,6 +51,13 @@ def _model_and_symbols(ix: SofaIndex, x: torch.Tensor, w, l: int):
     assert mism.sum() == 0, mism.sum()
 
 
+def _free_bytes() -> float:
+    """free device memory after dropping what earlier tests left in torch's cache"""
+    gc.collect()
+    torch.cuda.empty_cache()
+    return torch.cuda.mem_get_info()[0]
+
+
 def _run(name: str, check_model: bool = False):
     w = datagen.WORKLOADS[name]
     x = datagen.generate_rows(w, 0, w.n_series, device="cuda")
@@ -64,6 +73,8 @@ def _run(name: str, check_model: bool = False):
     assert_knn_parity(dn, inn, do, io)
     if check_model:
         _model_and_symbols(ix, x, w, w.l)
+    ix.close()
+    del x, q, d, i
     return st
 
 
@@ -82,7 +93,7 @@ def test_cfg3_full_size_every_query():
 def test_cfg4_full_size_every_query_one_gpu():
     """configs[3] on ONE GPU: 100M random walks (102.4 GB), 1000 noisy members, sigma 0.01/0.1/1.0
     (the sigma = 1 third included: no known answer there, the oracle decides)"""
-    free = torch.cuda.mem_get_info()[0]
+    free = _free_bytes()
     if free < 140e9:
         pytest.skip(f"needs ~140 GB free device memory, have {free / 1e9:.0f} GB")
     st = _run("cfg4", check_model=True)
@@ -92,7 +103,7 @@ def test_cfg4_full_size_every_query_one_gpu():
 def test_cfg5_full_size_every_query_one_gpu():
     """configs[4] at its real size on ONE GPU: 20M x 1024 (82 GB), half random walk / half high
     frequency, l = 32, 10-NN, 1000 queries"""
-    free = torch.cuda.mem_get_info()[0]
+    free = _free_bytes()
     if free < 120e9:
         pytest.skip(f"needs ~120 GB free device memory, have {free / 1e9:.0f} GB")
     st = _run("cfg5", check_model=True)
