@@ -57,7 +57,6 @@ def parse():
     return p.parse_args()
 
 
-TF32_PER_BF16 = 1.1 / 2.25  # nominal dense TF32 : BF16 tensor throughput (B200_PROFILING.md)
 HBM_NOMINAL_GBS = 8000.0    # BASELINE.json north_star "roughly 8 TB/s" (DGX figure; HGX 7.7)
 
 
@@ -79,14 +78,17 @@ def load_traffic(config: str) -> dict | None:
 
 
 def dense_roofline(st, km, rows, w, bf16, bf16_kind):
-    """dense pass (f1): 2 * queries * rows * n flops of the screen GEMM (the exact refine is tiny)"""
+    """dense pass (f1): 2 * queries * rows * n flops of the bf16 screen GEMM (tcgen05 kind::f16; the
+    exact refine of the candidates is tiny), against the measured bf16 rate"""
     flops = 2.0 * st["dense_queries"] * rows * w.length
-    tf32_peak = bf16 * TF32_PER_BF16
-    dn = {"bound": "tensor", "achieved": flops / (km["dense"] / 1e3) / 1e12, "peak": tf32_peak, "unit": "TFLOP/s",
-          "kernel": "k_dense_screen + k_dense_post (tcgen05 kind::tf32)", "group": "dense", "kernel_ms": km["dense"],
-          "algorithmic_flops_per_launch": flops,
-          "peak_note": f"{bf16_kind} {bf16:.1f} TFLOP/s x 1.1/2.25 (nominal dense TF32/BF16 ratio)"}
-    dn["frac"] = dn["achieved"] / tf32_peak
+    dn = {"bound": "tensor", "achieved": flops / (km["dense"] / 1e3) / 1e12, "peak": bf16, "unit": "TFLOP/s",
+          "kernel": "k_dense_screen + k_dense_post (tcgen05 kind::f16, bf16 operands)", "group": "dense",
+          "kernel_ms": km["dense"], "algorithmic_flops_per_launch": flops, "peak_note": f"{bf16_kind} {bf16:.1f} TFLOP/s",
+          "peak_nominal": 2250.0}
+    dn["frac"] = dn["achieved"] / bf16
+    dn["frac_nominal"] = dn["achieved"] / 2250.0
+    # the screen streams the rows' bf16 copy once per query group (2 n bytes per row)
+    dn["stream_bytes_per_group"] = rows * w.length * 2
     return dn
 
 

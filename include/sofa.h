@@ -244,8 +244,20 @@ typedef struct {
   int64_t n, n_blocks, global_offset, global_n;
   int32_t len, l, alphabet, block_size, word_stride;
   double build_ms[4];
+  int32_t dense_enabled;  /* 1 if the dense path is available (its bfloat16 row copy, n x len x 2 bytes,
+                             was allocated; 0 if disabled by opts or device memory) */
 } sofa_index_info;
 int sofa_get_info(const sofa_index* ix, sofa_index_info* out);
+
+/* Verification entry of the dense screen (reading 29): the tcgen05
+ * kind::f16 dot products the screen computes, for m rows and q queries given as float32 (rounded to
+ * bfloat16 to nearest inside, exactly as the index's row copy and the query prep round them), with
+ * no screening: out[i * q + j] = the fp32 tensor-core accumulation of bf16(rows[i]) . bf16(queries[j]).
+ * Lets a test measure the hardware's accumulation error against the bound the screen assumes.
+ *   rows_dev: m x len float32; queries_dev: q x len float32; out_dev: m x q float32 (device).
+ *   Synchronous.  Errors: EINVAL (m < 1, q < 1 or q > 256, bad len), ENOMEM, ECUDA. */
+int sofa_dense_dots(const float* rows_dev, int64_t m, int32_t len, const float* queries_dev, int32_t q,
+                    float* out_dev, void* cuda_stream);
 
 /* Copy the index arrays into caller device buffers (any may be NULL):
  * words_sorted n x word_stride uint8, perm n int32 (sorted position -> local row),

@@ -243,28 +243,32 @@ __device__ __forceinline__ uint64_t word_key(const uint8_t* w, int l, int a_bits
 
 }  // namespace sofa
 
-// Dense-path (f1) scratch, per index, grown on demand (dense.cu).  counters (16 ints):
-// [0] dense query slots, [1] overflowed slots, [2..3] candidate count (u64), [4] finished CTAs,
-// [6..7] estimated sparse refines of the flagged queries (u64, the batch decision).
+// Dense-path (f1) scratch, per index, grown on demand (dense.cu).  counters (64 ints): [0] dense query
+// slots, [1] overflowed slots, [2..3] candidate count (u64), [4] finished CTAs, [6..7] estimated
+// sparse refines of the flagged queries (u64, the batch decision); then 1024 ints of per-CTA progress.
 struct DenseScratch {
   int q_cap = 0, k_cap = 0, len = 0;
   int64_t cand_cap = 0;
-  float* qhat = nullptr;      // slot x len: z-normalised query (float32, same bits as the sparse path)
-  float4* qparams = nullptr;  // slot: (|q^|^2, sum q^, 2 gamma |q^|, refine slack)
-  int* qidx = nullptr;        // slot -> query index
-  float* binit = nullptr;     // slot -> caller's bound
-  float* bsf = nullptr;       // slot -> exact k-th best squared distance (or the bound)
-  float* thr = nullptr;       // slot -> screening threshold
-  float* tkd = nullptr;       // slot x k_cap
-  int* tki = nullptr;         // slot x k_cap (local rows)
+  float* qhat = nullptr;           // slot x len: z-normalised query (float32, same bits as the sparse path)
+  __nv_bfloat16* qb16 = nullptr;   // slot x xb_ld: the same, bfloat16 (the screen's B operand)
+  float4* qparams = nullptr;       // slot: (|q^|^2, eps, -, -)
+  int* qidx = nullptr;             // slot -> query index
+  float* binit = nullptr;          // slot -> caller's bound
+  float* bsf = nullptr;            // slot -> exact k-th best squared distance (or the bound)
+  float* thr = nullptr;            // slot -> proven bound on the k-th best (screening threshold)
+  float* tkd = nullptr;            // slot x k_cap
+  int* tki = nullptr;              // slot x k_cap (local rows)
   int* tkn = nullptr;
   int* lock = nullptr;
+  float* ubl = nullptr;            // slot x k_cap: k smallest upper bounds of candidate rows (k > 1)
+  int* ubn = nullptr;
+  int* ub_lock = nullptr;
   int* overflow = nullptr;
   int* ovf_list = nullptr;
   unsigned long long* cand = nullptr;
   int* counters = nullptr;
-  alignas(64) unsigned char tmap_q[128];  // CUtensorMap of qhat (q x len), encoded for tmap_q_rows rows
-  alignas(64) unsigned char tmap_x[128];  // CUtensorMap of the series (n x len)
+  alignas(64) unsigned char tmap_q[128];  // CUtensorMap of qb16, encoded for tmap_q_rows rows
+  alignas(64) unsigned char tmap_x[128];  // CUtensorMap of the index's bf16 rows
   int tmap_q_rows = -1;
 };
 
@@ -277,6 +281,8 @@ struct sofa_index {
   uint8_t* words = nullptr;       // n x WS, sorted by key
   float2* stats = nullptr;        // n, sorted order: (mu, 1/sigma)
   float2* stats_orig = nullptr;   // n, original row order (dense path)
+  __nv_bfloat16* xb16 = nullptr;  // n x xb_ld, original row order: z-normalised rows in bfloat16 (dense screen)
+  int xb_ld = 0;                  // row stride of xb16 (len rounded up to 8: 16-byte TMA rows)
   int32_t dense_permille = 100;   // dense path when >= this many permille of blocks survive (0: off)
   double build_ms[4] = {};        // model, transform, sort, gather + envelopes (CUDA events)
   DenseScratch dense;
@@ -341,6 +347,7 @@ int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_
 inline int64_t dense_batch_rows(const sofa_index* ix) { return ix->n > 0 ? ix->n : 1; }
 int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stats, cudaStream_t st);
 int ensure_dense_scratch(sofa_index* ix, int q, int k);
+int dense_dots(const float* rows, int64_t m, int len, const float* queries, int q, float* out, cudaStream_t st);
 void free_dense_scratch(sofa_index* ix);
 int launch_merge(const float* d, const int64_t* i, int parts, int q, int k, float* od, int64_t* oi, cudaStream_t st);
 int launch_fill_pad(float* od, int64_t* oi, int64_t cnt, cudaStream_t st);

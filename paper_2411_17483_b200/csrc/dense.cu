@@ -2,47 +2,53 @@
 //
 // GEMINI filters with a lower bound and verifies with the true distance.  When a
 // query's envelope filter (a6) keeps most blocks even after its lowest-LB blocks have been
-// refined (high-frequency data: SURVEY SIM-3b, TLB 0.24, ~99.5% of series survive), refining
-// "every survivor" means streaming the whole dataset once PER QUERY.  Such queries are batched
-// here instead and given a second lower bound that is cheap in bulk:
+// refined (high-frequency data: SURVEY SIM-3b, TLB 0.24, ~99.5% of series survive; random walks
+// with sigma = 1 noise: ~15% refined), refining "every survivor" means streaming the dataset once
+// PER QUERY.  Such queries are batched here instead and given a second lower bound that is cheap
+// in bulk:
 //
-//   dot(q^, x)   tensor-core TF32 GEMM (tcgen05.mma kind::tf32, fp32 accumulate in TMEM) of the
-//                z-normalised queries (M = 128 per tile) against the RAW float32 rows (N = 256
-//                per tile), both TMA-loaded straight from HBM (no conversion pass);
-//   x^.q^        = inv_sigma * (dot - mu * sum(q^))                  (z-norm on the fly, a1)
-//   approx d^2   = |q^|^2 + |x^|^2 - 2 x^.q^
-//   |error|     <= eps = 2 gamma |q^| inv_sigma |x| + r  (TF32 operand truncation 2^-10 each,
-//                 fp32 accumulation, and r = slack for the refine's own float32 rounding)
-//   LB_g = approx - eps <= exact d^2 <= approx + eps = UB_g.
+//   dot(x^, q^)  tensor-core bf16 GEMM (tcgen05.mma kind::f16, fp32 accumulate in TMEM) of the
+//                z-normalised ROWS (M = 128 per tile, a bfloat16 copy written by the build's
+//                transform, original row order, TMA-streamed once per query group) against the
+//                z-normalised queries (N <= 256 per group, bfloat16, resident in shared memory);
+//   approx d^2   = |q^|^2 + |x^|^2 - 2 dot,  |x^|^2 = n (0 for a constant row);
+//   |error|     <= eps_q = 2 gamma sqrt(1.0001 n) |q^| + 2e-4 (|q^|^2 + n) + 1e-3 with
+//                 gamma = 2^-7 + 2^-15 + n 2^-23 (each bf16 operand rounds by <= 2^-8 relative,
+//                 products exact, fp32 accumulation bounded as a naive sum and doubled), and the
+//                 slack covering |x^|^2 = n only to the float32 statistics and the refine's own
+//                 float32 rounding (reading 29; pinned on CPU by tests/test_dense_bound.py,
+//                 and the tensor cores' accumulation measured against it by test_gpu_dense.py);
+//   LB_g = approx - eps <= d2_refine <= approx + eps = UB_g.
 //
-// A row is a candidate iff LB_g <= thr_q, where thr_q is the smallest proven upper bound on the
-// query's k-th best distance: the exact k-th best so far (seed block, refined candidates), or the
-// k-th smallest UB_g a thread has seen (k distinct rows), shared across CTAs by atomicMin.
-// Candidates are then refined EXACTLY by the same ed_warp_multi arithmetic as the sparse path (a8),
-// so the dense path returns bit-identical distances.  Exactness: every true top-k row x* has
-// LB_g(x*) <= d^2(x*) <= true k-th <= thr_q at all times, so it is always emitted.
+// A row is a candidate iff LB_g <= thr_q, thr_q being a proven upper bound on the query's k-th
+// best: the exact k-th best of the rows the front refined, lowered during the pass by the k-th
+// smallest UB_g of candidate rows (a row that could lower it is itself a candidate, so only
+// candidates need tracking).  Candidates are refined EXACTLY by the same ed_warp_multi arithmetic
+// as the sparse path (a8), so the dense path returns bit-identical distances.  Exactness: every
+// true top-k row x* has LB_g(x*) <= d2(x*) <= true k-th <= thr_q at all times, so it is emitted.
 //
-// Kernels: k_dense_screen (warp-specialised tcgen05 GEMM + screening epilogue, persistent, one
-// CTA per SM) and k_dense_post (exact refine of the candidates, brute-force fallback for a query
-// whose candidates overflowed the buffer, then the last CTA writes the dense queries' outputs).
+// Kernels: k_dense_screen (warp-specialised tcgen05 GEMM + screening epilogue, persistent, one CTA
+// per SM, cooperative launch) and k_dense_post (exact refine of the candidates, brute-force fallback
+// for a query whose candidates overflowed the buffer, then the last CTA writes the outputs).
+// Queries are split into groups of at most NQmax (TMEM: 2 x 256 accumulator columns; shared
+// memory: the group's queries stay resident); the CTAs of different groups that stream the same
+// row tiles stay within a few tiles of each other (their "twins"), so a tile read from HBM by one is
+// re-read from L2 by the others.  The cooperative launch guarantees the twins are co-resident.
 #include <cudaTypedefs.h>
 
-#include <cstdlib>
+#include <cuda_bf16.h>
 
 #include "common.cuh"
 
 namespace sofa {
 
-constexpr int DM = 128;                 // queries per tile  (MMA M = TMEM lanes)
-constexpr int DN = 256;                 // series per tile   (MMA N = accumulator columns)
-constexpr int DKC = 32;                 // fp32 per K chunk = 128-byte rows (SWIZZLE_128B atom)
-constexpr int DSTAGES = 4;              // TMA -> MMA pipeline depth
-constexpr int DA_BYTES = DM * DKC * 4;  // 16 KB
-constexpr int DB_BYTES = DN * DKC * 4;  // 32 KB
-constexpr int D_THREADS = 320;          // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2..9 epilogue
-constexpr int D_UBK = SOFA_MAX_K;       // k-th-smallest UB tracking (local memory; updates are rare)
-constexpr int D_AHEAD_CHUNKS = 64;      // K-chunks a CTA may run ahead of the others reading its series tiles
-constexpr size_t D_SMEM = 1024 + DSTAGES * (DA_BYTES + DB_BYTES) + 2 * DN * 8 + 64 + 256;
+constexpr int DM = 128;                  // rows per tile (MMA M = TMEM lanes)
+constexpr int DKC = 64;                  // bf16 per K chunk = 128-byte rows (SWIZZLE_128B atom)
+constexpr int DA_BYTES = DM * DKC * 2;   // 16 KB per A stage
+constexpr int D_THREADS = 320;           // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2..9 epilogue
+constexpr int D_AHEAD = 3;               // row tiles a CTA may run ahead of its twins
+constexpr int D_SMEM_MAX = 232448;       // opt-in shared memory per CTA on sm_100
+constexpr int D_MISC = 4096;             // per-query thresholds / norms + barriers
 
 // ------------------------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -80,11 +86,11 @@ __device__ __forceinline__ void tc_commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
                : "memory");
 }
-// D[tmem] (+)= A[smem] . B[smem]^T, kind::tf32, both operands K-major
-__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+// D[tmem] (+)= A[smem] . B[smem]^T, kind::f16 (bf16 operands, fp32 accumulate), both K-major
+__device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                             uint32_t accumulate) {
   asm volatile(
-      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
@@ -94,36 +100,42 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-// instruction descriptor: D f32 (bits 4-5 = 1), A/B tf32 (bits 7-9, 10-12 = 2), K-major both,
-// N >> 3 at bits 17-22, M >> 4 at bits 24-28.
-constexpr uint32_t kIdescTF32 =
-    (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(DN >> 3) << 17) | ((uint32_t)(DM >> 4) << 24);
+// instruction descriptor, kind::f16: D f32 (bits 4-5 = 1), A/B bf16 (bits 7-9, 10-12 = 1), both
+// K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28 (cute/arch/mma_sm100_desc.hpp layout)
+__device__ __forceinline__ uint32_t idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(DM >> 4) << 24);
+}
 
-#define TMEM_LD32(addr, r)                                                                                        \
-  asm volatile(                                                                                                   \
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19," \
-      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                                   \
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),           \
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),     \
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),   \
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])    \
-      : "r"(addr))
+#define TMEM_LD16(addr, r)                                                                                 \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),   \
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),          \
+                 "=r"(r[15])                                                                                       \
+               : "r"(addr))
 
 struct DenseArgs {
   int64_t n, dense_rows;
   int len, k, KC;
   int64_t n_tiles;
+  int nq_max;                // queries per group (shared memory / TMEM limit of this launch)
+  int stages;                // A ring depth
   const float2* stats_orig;  // (mu, inv_sigma) per original row
   const int* qd_count;       // number of dense query slots (device)
-  const float4* qparams;     // per slot: (|q^|^2, sum q^, 2 gamma |q^|, 2e-4 |q^|^2 + 1e-3)
-  float* thr;                // per slot: screening threshold (>= true k-th best), atomicMin as uint
+  const float4* qparams;     // per slot: (|q^|^2, eps, -, -)
+  float* thr;                // per slot: proven bound on the k-th best (atomicMin as uint)
+  float* ubl;                // per slot: k smallest UB_g of candidate rows (k > 1), under ub_lock
+  int* ubn;
+  int* ub_lock;
   unsigned long long* cand;  // (slot << 32) | row
   int64_t cand_cap;
   unsigned long long* cand_count;
   int* overflow;  // per slot flag
   int* ovf_list;
   int* ovf_count;
-  int* progress;  // per CTA: items whose loads are issued (zeroed per call)
+  int* progress;  // per CTA: row tiles whose loads are issued (zeroed per call)
+  float* raw_out; // debug (sofa_dense_dots): write the raw dot products, rows x raw_ld, no screening
+  int raw_ld;
+  int raw_q;      // debug: number of query slots (instead of *qd_count)
 };
 
 __device__ __forceinline__ void emit_candidate(const DenseArgs& A, bool pass, int slot, uint32_t row) {
@@ -143,61 +155,85 @@ __device__ __forceinline__ void emit_candidate(const DenseArgs& A, bool pass, in
   }
 }
 
-// k-th-smallest insertion for k > 1 (rare after the item's first k rows; kept out of line so the
-// unrolled element loop stays small)
-__device__ __noinline__ void ub_insert(float* ubl, int& nub, float& ubk, int kk, float ap) {
-  int p = nub < kk ? nub : kk - 1;
-  while (p > 0 && ubl[p - 1] > ap) {
-    ubl[p] = ubl[p - 1];
-    --p;
+// shared-memory float minimum (values of either sign), rare path
+__device__ __forceinline__ void smem_fmin(float* p, float v) {
+  int* ip = reinterpret_cast<int*>(p);
+  int old = *ip;
+  while (v < __int_as_float(old)) {
+    const int prev = atomicCAS(ip, old, __float_as_int(v));
+    if (prev == old) break;
+    old = prev;
   }
-  ubl[p] = ap;
-  if (nub < kk) ++nub;
-  if (nub == kk) ubk = ubl[kk - 1];
 }
 
-// The j-th item (query tile m, series tile t) of this CTA.  When the grid holds at least one CTA
-// per query tile, CTA b serves tile m = b % mt only (so per-query state persists across its items)
-// and the CTAs sharing a series tile t run together (its rows are read from HBM once, then L2).
-__device__ __forceinline__ bool dense_item(int64_t j, int64_t mt, int64_t n_tiles, int& m, int64_t& t) {
-  const int64_t G = gridDim.x, b = blockIdx.x;
-  if (mt <= G) {
-    const int64_t per = G / mt;
-    if (b >= per * mt) return false;
-    m = (int)(b % mt);
-    t = b / mt + j * per;
-    return t < n_tiles;
+// a candidate row's upper bound UB_g lowers the query's threshold: k = 1 directly; k > 1 through
+// the k smallest UBs of distinct candidate rows (each row is screened once per query)
+__device__ void offer_ub(const DenseArgs& A, int slot, float ub, float* s_d, float eps_minus_qn) {
+  float t = INFINITY;
+  if (A.k == 1) {
+    t = ub;
+  } else {
+    int* lk = &A.ub_lock[slot];
+    while (atomicCAS(lk, 0, 1) != 0) {
+    }
+    __threadfence();
+    volatile float* l = A.ubl + (int64_t)slot * A.k;
+    const int n = *(volatile int*)&A.ubn[slot];
+    if (n < A.k || ub < l[n - 1]) {
+      int p = n < A.k ? n : A.k - 1;
+      while (p > 0 && l[p - 1] > ub) {
+        l[p] = l[p - 1];
+        --p;
+      }
+      l[p] = ub;
+      const int nn = n < A.k ? n + 1 : A.k;
+      *(volatile int*)&A.ubn[slot] = nn;
+      if (nn == A.k) t = l[A.k - 1];
+    }
+    __threadfence();
+    atomicExch(lk, 0);
   }
-  const int64_t it = b + j * G;
-  m = (int)(it % mt);
-  t = it / mt;
-  return t < n_tiles;
+  if (t < INFINITY) {
+    atomicMin(reinterpret_cast<unsigned int*>(&A.thr[slot]), __float_as_uint(t));
+    smem_fmin(s_d, t + eps_minus_qn);
+  }
 }
 
-template <bool KONE>
+// Row tiles of CTA b: with g query groups and c = G / g CTAs per group, CTA b serves group b % g and
+// row tiles (b / g) + j c; CTAs b >= c g idle.  "Twins": CTAs with the same b / g (same tiles).
 __global__ void __launch_bounds__(D_THREADS, 1)
-    k_dense_screen(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX, const DenseArgs A) {
+    k_dense_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const DenseArgs A) {
   extern __shared__ __align__(1024) unsigned char dsm_raw[];
   unsigned char* dsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* sA = dsm;
-  unsigned char* sB = dsm + DSTAGES * DA_BYTES;
-  float2* s_ser2 = reinterpret_cast<float2*>(sB + DSTAGES * DB_BYTES);  // [2][DN]
-  float* s_tmax = reinterpret_cast<float*>(s_ser2 + 2 * DN);              // [2][4]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_tmax + 8);
-  uint64_t* full = bars;                    // [DSTAGES]
-  uint64_t* empty = bars + DSTAGES;         // [DSTAGES]
-  uint64_t* tfull = bars + 2 * DSTAGES;     // [2]
-  uint64_t* tempty = bars + 2 * DSTAGES + 2;  // [2]
   __shared__ uint32_t s_tmem;
+  __shared__ uint64_t bars[2 * 8 + 5];
 
-  const int qd = *A.qd_count;
-  if (qd == 0 || *reinterpret_cast<const unsigned long long*>(A.qd_count + 6) < (unsigned long long)A.dense_rows)
+  const int qd = A.raw_out ? A.raw_q : *A.qd_count;
+  if (qd == 0) return;
+  if (!A.raw_out && *reinterpret_cast<const unsigned long long*>(A.qd_count + 6) < (unsigned long long)A.dense_rows)
     return;  // batch decision: sparse (the deferred k_query launch finishes the flagged queries)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t mt = (qd + DM - 1) / DM;
+  const int ng = (qd + A.nq_max - 1) / A.nq_max;               // query groups
+  const int nq = ((qd + ng - 1) / ng + 15) / 16 * 16;          // columns per group (MMA N), <= nq_max
+  const int G = gridDim.x, b = blockIdx.x;
+  const int cpg = G / ng;
+  if (b >= cpg * ng) return;                                   // (only with more groups than CTAs / group)
+  const int grp = b % ng, twin = b / ng;
+  const int q0 = grp * nq, nqv = qd - q0 < nq ? qd - q0 : nq;  // valid columns of this group
+  const int S = A.stages, KC = A.KC;
+  unsigned char* sB = dsm;                                     // KC x nq x 128 B (resident)
+  unsigned char* sA = dsm + (size_t)KC * A.nq_max * 128;       // S x 16 KB
+  float* s_d = reinterpret_cast<float*>(sA + (size_t)S * DA_BYTES);  // nq: thr + eps - |q^|^2
+  float* s_qn = s_d + 256;                                            // nq: |q^|^2
+  float* s_eps = s_qn + 256;                                          // nq: eps
+  uint64_t* full = bars;           // [S]
+  uint64_t* empty = bars + 8;      // [S]
+  uint64_t* tfull = bars + 16;     // [2]
+  uint64_t* tempty = bars + 18;    // [2]
+  uint64_t* bfull = bars + 20;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < DSTAGES; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -205,10 +241,22 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 8 * 32);
     }
+    mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
-    for (int i = 0; i < 8; ++i) s_tmax[i] = 0.f;
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  for (int c = threadIdx.x; c < 256; c += D_THREADS) {
+    float d = -INFINITY, qn = 0.f, e = 0.f;
+    if (c < nqv && !A.raw_out) {
+      const float4 qp = A.qparams[q0 + c];
+      qn = qp.x;
+      e = qp.y;
+      d = *(volatile float*)&A.thr[q0 + c] + e - qn;  // +inf while fewer than k rows are known
+    }
+    s_d[c] = d;
+    s_qn[c] = qn;
+    s_eps[c] = e;
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem))
@@ -219,71 +267,69 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
+  const int64_t T = A.n_tiles;
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
+      // the group's queries: every K chunk, 16 rows per box, resident for the whole pass
+      mbar_expect_tx(bfull, (uint32_t)(KC * nq * 128));
+      for (int kc = 0; kc < KC; ++kc)
+        for (int r = 0; r < nq; r += 16) tma_load_2d(sB + ((size_t)kc * A.nq_max + r) * 128, &tmB, kc * DKC, q0 + r, bfull);
+      volatile int* prog = A.progress;
       int stage = 0;
       uint32_t phase = 0;
-      int m;
-      int64_t t;
-      // the CTAs that read the same series tiles (one per query tile) stay within a few items of each
-      // other, so a tile fetched from HBM by one of them is still in L2 for the others
-      const int64_t G = gridDim.x, b = blockIdx.x;
-      const bool grouped = mt > 1 && mt <= G && b < (G / mt) * mt;
-      const int64_t g0 = grouped ? (b / mt) * mt : 0;
-      volatile int* prog = A.progress;
-      // slack in items: about D_AHEAD_CHUNKS K-chunks (short items get a wider window)
-      const int64_t ahead = A.KC >= D_AHEAD_CHUNKS / 2 ? 2 : D_AHEAD_CHUNKS / A.KC;
       int64_t j = 0;
-      for (; dense_item(j, mt, A.n_tiles, m, t); ++j) {
-        if (grouped && j > ahead && j % (ahead / 2 > 0 ? ahead / 2 : 1) == 0) {
-          for (;;) {  // all members' progress loaded together, then compared
+      for (int64_t t = twin; t < T; t += cpg, ++j) {
+        if (ng > 1) {  // stay within D_AHEAD tiles of the twins (the tile is then still in L2 for them)
+          for (;;) {
             int lo = 0x7fffffff;
-            for (int64_t o = 0; o < mt; ++o) {
-              const int p = prog[g0 + o];
+            for (int o = 0; o < ng; ++o) {
+              const int p = prog[twin * ng + o];
               lo = p < lo ? p : lo;
             }
-            if (lo >= j - ahead) break;
-            __nanosleep(128);
+            if (lo >= j - D_AHEAD) break;
+            __nanosleep(256);
           }
         }
-        for (int kc = 0; kc < A.KC; ++kc) {
+        for (int kc = 0; kc < KC; ++kc) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], DA_BYTES + DB_BYTES);
-          tma_load_2d(sA + stage * DA_BYTES, &tmQ, kc * DKC, m * DM, &full[stage]);
-          tma_load_2d(sB + stage * DB_BYTES, &tmX, kc * DKC, (int)(t * DN), &full[stage]);
-          if (++stage == DSTAGES) {
+          mbar_expect_tx(&full[stage], DA_BYTES);
+          tma_load_2d(sA + stage * DA_BYTES, &tmA, kc * DKC, (int)(t * DM), &full[stage]);
+          if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        prog[b] = (int)(j + 1);  // items whose loads this CTA has issued
+        prog[b] = (int)(j + 1);
       }
-      prog[b] = 0x7fffffff;  // done: never holds the group back
+      prog[b] = 0x7fffffff;  // done: never holds a twin back
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer (one thread)
     if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(nq);
+      mbar_wait(bfull, 0);
+      tc_fence_after();
       int stage = 0;
       uint32_t phase = 0;
-      int m;
-      int64_t t, local = 0;
-      for (int64_t j = 0; dense_item(j, mt, A.n_tiles, m, t); ++j, ++local) {
-        const int acc = (int)(local & 1);
-        const uint32_t aph = (uint32_t)((local >> 1) & 1);
+      int64_t j = 0;
+      for (int64_t t = twin; t < T; t += cpg, ++j) {
+        const int acc = (int)(j & 1);
+        const uint32_t aph = (uint32_t)((j >> 1) & 1);
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
-        const uint32_t dt = tmem + (uint32_t)(acc * DN);
-        for (int kc = 0; kc < A.KC; ++kc) {
+        const uint32_t dt = tmem + (uint32_t)(acc * 256);
+        for (int kc = 0; kc < KC; ++kc) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * DA_BYTES), b0 = smem_u32(sB + stage * DB_BYTES);
+          const uint32_t a0 = smem_u32(sA + stage * DA_BYTES);
+          const uint32_t b0 = smem_u32(sB + (size_t)kc * A.nq_max * 128);
 #pragma unroll
-          for (int kk = 0; kk < DKC / 8; ++kk)  // UMMA_K = 8 tf32 = 32 bytes along the swizzled row
-            tc_mma_tf32(dt, sdesc_sw128(a0 + 32 * kk), sdesc_sw128(b0 + 32 * kk), kIdescTF32, (kc | kk) ? 1u : 0u);
+          for (int kk = 0; kk < DKC / 16; ++kk)  // UMMA_K = 16 bf16 = 32 bytes along the swizzled row
+            tc_mma_bf16(dt, sdesc_sw128(a0 + 32 * kk), sdesc_sw128(b0 + 32 * kk), idesc, (kc | kk) ? 1u : 0u);
           tc_commit(&empty[stage]);
-          if (++stage == DSTAGES) {
+          if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
@@ -293,127 +339,68 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     }
   } else {
     // ---------------------------------------------------------------- epilogue (8 warps)
-    // warp w reads TMEM lane quarter w % 4 (query rows) and column half (w - 2) / 4 (series).
-    // Per element: approx' = -2 inv dot + |q^|^2 + |x^|^2 (2 ops); the per-row error terms are
-    // replaced by their maximum over the tile's rows (a valid, marginally looser bound):
-    //   eps_max = 2 gamma |q^| max_s(inv |x|) + slack_q + max_s(slack_s) + |sum q^| max_s|2 mu inv|
-    // (the last term covers dropping +2 mu inv sum(q^) from approx').  LB = approx' - eps_max,
-    // UB = approx' + eps_max.
-    const int eq = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const int row = eq * 32 + lane;
-    const int et = (warp - 2) * 32 + lane;  // 0..255: one series of the tile each in the fill
+    // warp w reads TMEM lane quarter w % 4 (its 32 rows of the tile) and every other 16-column chunk
+    // (half (w - 2) / 4).  Per element: val = 2 dot + (thr + eps - |q^|^2); the row is a candidate
+    // for that query iff val >= |x^|^2 (LB_g <= thr).
+    const int qtr = warp & 3, half = (warp - 2) >> 2;
+    const int r = qtr * 32 + lane;
+    const int nch = nq / 16;
     const float nlen = (float)A.len;
-    // per thread (one query row): the k smallest UB_g it has seen, kept across all of the CTA's items
-    // (the grid is a multiple of the number of query tiles, so a CTA always serves the same tile)
-    const int kk = A.k;
-    const bool track = kk <= D_UBK;
-    float ubk = INFINITY;  // k-th smallest UB seen: a proven bound on the query's k-th best
-    float ubl[D_UBK];
-    int nub = 0;
-    int cur_m = -1, m;
-    int64_t t, local = 0;
-    for (int64_t j = 0; dense_item(j, mt, A.n_tiles, m, t); ++j, ++local) {
-      if (m != cur_m) {  // only with more query tiles than CTAs
-        cur_m = m;
-        ubk = INFINITY;
-        nub = 0;
-      }
-      const int acc = (int)(local & 1);
-      const uint32_t aph = (uint32_t)((local >> 1) & 1);
-      float2* ser = s_ser2 + acc * DN;     // (-2 inv, |x^|^2), NaN |x^|^2 past the last row
-      float* tmx = s_tmax + acc * 4;      // tile maxima: inv |x|, slack_s, |2 mu inv|
-      {
-        const int64_t s = t * DN + et;
-        // past the last row: NaN, never <= any threshold (+inf would pass an infinite one, i.e.
-        // while a query holds fewer than k results)
-        float2 v = make_float2(0.f, __int_as_float(0x7fffffff));
-        float e = 0.f, rs = 0.f, b = 0.f;
-        if (s < A.n) {
-          const float2 st = A.stats_orig[s];
-          v = make_float2(0.f, 0.f);
-          if (st.y > 0.f) {
-            const float mi = st.x * st.y;
-            v = make_float2(-2.f * st.y, nlen);
-            e = sqrtf(nlen * (1.f + mi * mi)) * 1.0001f;
-            rs = fmaf(2.4e-7f, e * e, 2e-4f * nlen);
-            b = fabsf(2.f * mi);
-          }
-        }
-        ser[et] = v;
-        // max over the tile's rows (non-negative floats order like their bit patterns)
-        e = fmaxf(e, __shfl_xor_sync(FULL, e, 16)); rs = fmaxf(rs, __shfl_xor_sync(FULL, rs, 16));
-        b = fmaxf(b, __shfl_xor_sync(FULL, b, 16));
-#pragma unroll
-        for (int o = 8; o >= 1; o >>= 1) {
-          e = fmaxf(e, __shfl_xor_sync(FULL, e, o));
-          rs = fmaxf(rs, __shfl_xor_sync(FULL, rs, o));
-          b = fmaxf(b, __shfl_xor_sync(FULL, b, o));
-        }
-        if (lane == 0) {
-          atomicMax(reinterpret_cast<unsigned int*>(&tmx[0]), __float_as_uint(e));
-          atomicMax(reinterpret_cast<unsigned int*>(&tmx[1]), __float_as_uint(rs));
-          atomicMax(reinterpret_cast<unsigned int*>(&tmx[2]), __float_as_uint(b));
-        }
-      }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      const int slot = m * DM + row;
-      const bool qv = slot < qd;
-      const float4 qp = qv ? A.qparams[slot] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float eps = fmaf(qp.z, tmx[0], qp.w + tmx[1]) + fabsf(qp.y) * tmx[2];
-      float thr = qv ? fminf(*(volatile float*)&A.thr[slot], ubk) : -INFINITY;
-      float thr_e = thr + eps;
-      float ubk_ap = ubk - eps;  // a row improves the UB list iff approx' < ubk - eps
+    int64_t j = 0;
+    for (int64_t t = twin; t < T; t += cpg, ++j) {
+      const int acc = (int)(j & 1);
+      const uint32_t aph = (uint32_t)((j >> 1) & 1);
+      const int64_t row = t * DM + r;
+      float xn = __int_as_float(0x7fffffff);  // past the last row: NaN, never a candidate
+      if (row < A.n) xn = A.stats_orig[row].y > 0.f ? nlen : 0.f;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const uint32_t tbase = tmem + ((uint32_t)(eq * 32) << 16) + (uint32_t)(acc * DN + half * (DN / 2));
-      uint32_t r[2][32];
-      TMEM_LD32(tbase, r[0]);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const uint32_t tbase = tmem + ((uint32_t)(qtr * 32) << 16) + (uint32_t)(acc * 256);
+      for (int ch = half; ch < nch; ch += 2) {
+        uint32_t v[16];
+        TMEM_LD16(tbase + ch * 16, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int c0 = ch * 16;
+        if (A.raw_out) {
+          if (row < A.n)
+            for (int c = 0; c < 16; ++c)
+              if (c0 + c < nqv) A.raw_out[row * A.raw_ld + q0 + c0 + c] = __uint_as_float(v[c]);
+          continue;
+        }
+        float vmax = -INFINITY;
+        float val[16];
 #pragma unroll
-      for (int c = 0; c < DN / 64; ++c) {
-        uint32_t (&cur)[32] = r[c & 1];
-        if (c + 1 < DN / 64) TMEM_LD32(tbase + (c + 1) * 32, r[(c + 1) & 1]);  // next chunk in flight
-        const int col0 = half * (DN / 2) + c * 32;
-        float amin = INFINITY;
+        for (int c = 0; c < 16; c += 4) {
+          const float4 d4 = *reinterpret_cast<const float4*>(s_d + c0 + c);
+          val[c + 0] = fmaf(2.f, __uint_as_float(v[c + 0]), d4.x);
+          val[c + 1] = fmaf(2.f, __uint_as_float(v[c + 1]), d4.y);
+          val[c + 2] = fmaf(2.f, __uint_as_float(v[c + 2]), d4.z);
+          val[c + 3] = fmaf(2.f, __uint_as_float(v[c + 3]), d4.w);
+          vmax = fmaxf(vmax, fmaxf(fmaxf(val[c], val[c + 1]), fmaxf(val[c + 2], val[c + 3])));
+        }
+        if (__any_sync(FULL, vmax >= xn)) {  // rare: this chunk has candidates
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float2 sv = ser[col0 + j];
-          const float ap = fmaf(sv.x, __uint_as_float(cur[j]), qp.x + sv.y);
-          cur[j] = __float_as_uint(ap);
-          amin = fminf(amin, ap);
-          if constexpr (!KONE) {
-            if (track && ap < ubk_ap) {
-              ub_insert(ubl, nub, ubk, kk, ap + eps);
-              ubk_ap = ubk - eps;
+          for (int c = 0; c < 16; ++c) {
+            const bool pass = val[c] >= xn;
+            if (!__any_sync(FULL, pass)) continue;
+            const int col = c0 + c;
+            emit_candidate(A, pass, q0 + col, (uint32_t)row);
+            if (pass) {
+              const float dot = __uint_as_float(v[c]);
+              const float ub = (s_qn[col] + xn - 2.f * dot) + s_eps[col];
+              offer_ub(A, q0 + col, ub, s_d + col, s_eps[col] - s_qn[col]);
             }
           }
         }
-        if (__any_sync(FULL, amin <= thr_e)) {  // rare: emit this chunk's candidates (compact code)
-          uint32_t pass = 0;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) pass |= (__uint_as_float(cur[j]) <= thr_e ? 1u : 0u) << j;
-          while (__any_sync(FULL, pass != 0)) {
-            const int j = pass ? __ffs(pass) - 1 : 0;
-            emit_candidate(A, pass != 0, slot, (uint32_t)(t * DN + col0 + j));
-            pass &= pass - 1;
-          }
-        }
-        if constexpr (KONE) ubk = fminf(ubk, amin + eps);
-        thr = fminf(thr, fmaxf(ubk, 0.f));
-        thr_e = thr + eps;
-        if (c + 1 < DN / 64) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if (qv && thr >= 0.f && thr < INFINITY) {
-        const float g = *(volatile float*)&A.thr[slot];
-        if (thr < g) atomicMin(reinterpret_cast<unsigned int*>(&A.thr[slot]), __float_as_uint(thr));
-      }
-      // reset this buffer's tile maxima for its next use (two items later, after the bar.sync of
-      // the next item every thread has read them)
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      if (et < 4) tmx[et] = 0.f;
+      // other CTAs' improvements of the thresholds (global) into this CTA's copy
+      if (qtr == 0 && !A.raw_out)
+        for (int c = lane + 32 * half; c < nqv; c += 64) {
+          const float nd = *(volatile float*)&A.thr[q0 + c] + s_eps[c] - s_qn[c];
+          if (nd < s_d[c]) smem_fmin(s_d + c, nd);
+        }
     }
   }
   __syncthreads();
@@ -549,29 +536,33 @@ __global__ void __launch_bounds__(kThreads) k_dense_post(const DensePost P) {
 
 // ------------------------------------------------------------------------------------------------ host
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  static std::atomic<PFN_cuTensorMapEncodeTiled_v12000> fn{nullptr};
+  PFN_cuTensorMapEncodeTiled_v12000 f = fn.load();
+  if (!f) {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        q == cudaDriverEntryPointSuccess) {
+      f = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+      fn.store(f);
+    }
   }
-  return fn;
+  return f;
 }
 
-// rows x len float32 row-major, box = 32 fp32 (128 B, swizzled) x box_rows
-static int make_tmap(CUtensorMap* m, const float* base, int64_t rows, int len, int box_rows) {
+// rows x len bfloat16, row stride ld elements (ld % 8 == 0), box = 64 bf16 (128 B, swizzled) x box_rows;
+// elements past len / rows read as zero
+static int make_tmap_bf16(CUtensorMap* m, const __nv_bfloat16* base, int64_t rows, int len, int ld, int box_rows) {
   auto enc = encode_fn();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return SOFA_ECUDA;
   }
   cuuint64_t dims[2] = {(cuuint64_t)len, (cuuint64_t)(rows > 0 ? rows : 1)};
-  cuuint64_t strides[1] = {(cuuint64_t)len * 4};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
   cuuint32_t box[2] = {(cuuint32_t)DKC, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(base), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -581,27 +572,69 @@ static int make_tmap(CUtensorMap* m, const float* base, int64_t rows, int len, i
   return SOFA_OK;
 }
 
-int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stats, cudaStream_t st) {
-  DenseScratch& D = ix->dense;
-  int rc;
-  if (D.tmap_q_rows != q) {  // tensor maps are encoded once per buffer (not on every call)
-    if ((rc = make_tmap(reinterpret_cast<CUtensorMap*>(D.tmap_q), D.qhat, q, ix->len, DM))) return rc;
-    if ((rc = make_tmap(reinterpret_cast<CUtensorMap*>(D.tmap_x), ix->series, ix->n, ix->len, DN))) return rc;
-    D.tmap_q_rows = q;
+// launch geometry of the screen for row length `len`: A ring depth and the queries per group that fit
+// next to it (multiple of 16, <= 256 for the 2 x 256 TMEM accumulator columns)
+static void dense_geometry(int len, int& stages, int& nq_max) {
+  const int KC = (len + DKC - 1) / DKC;
+  nq_max = 0;
+  stages = 4;
+  for (int s = 4; s >= 2; --s) {
+    const int avail = D_SMEM_MAX - 1024 - s * DA_BYTES - D_MISC;
+    int nq = avail / (KC * 128) / 16 * 16;
+    if (nq > 256) nq = 256;
+    if (nq > nq_max) {
+      nq_max = nq;
+      stages = s;
+    }
+    if (nq >= 256) break;
   }
-  const CUtensorMap& tmQ = *reinterpret_cast<const CUtensorMap*>(D.tmap_q);
-  const CUtensorMap& tmX = *reinterpret_cast<const CUtensorMap*>(D.tmap_x);
-  DenseArgs A{};
+}
+
+static size_t dense_smem(int len, int stages, int nq_max) {
+  const int KC = (len + DKC - 1) / DKC;
+  return 1024 + (size_t)KC * nq_max * 128 + (size_t)stages * DA_BYTES + D_MISC;
+}
+
+static int launch_screen(sofa_index* ix, const CUtensorMap& tmA, const CUtensorMap& tmB, const DenseArgs& A,
+                         size_t smem, cudaStream_t st) {
+  static std::atomic<uint32_t> attr_set{0};  // per device: the smem attribute is set once
+  const uint32_t bit = 1u << (ix->device & 31);
+  if (!(attr_set.load() & bit)) {
+    SOFA_CK(cudaFuncSetAttribute(k_dense_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, D_SMEM_MAX));
+    attr_set.fetch_or(bit);
+  }
+  // cooperative: every CTA resident at once (the twins wait on each other's progress)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ix->sms);
+  cfg.blockDim = dim3(D_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  SOFA_CK(cudaLaunchKernelEx(&cfg, k_dense_screen, tmA, tmB, A));
+  SOFA_LAUNCHED();
+  return SOFA_OK;
+}
+
+static void fill_screen_args(sofa_index* ix, int k, DenseArgs& A) {
+  DenseScratch& D = ix->dense;
   A.n = ix->n;
   A.dense_rows = dense_batch_rows(ix);
   A.len = ix->len;
   A.k = k;
   A.KC = (ix->len + DKC - 1) / DKC;
-  A.n_tiles = (ix->n + DN - 1) / DN;
+  A.n_tiles = (ix->n + DM - 1) / DM;
+  dense_geometry(ix->len, A.stages, A.nq_max);
   A.stats_orig = ix->stats_orig;
   A.qd_count = D.counters;
   A.qparams = D.qparams;
   A.thr = D.thr;
+  A.ubl = D.ubl;
+  A.ubn = D.ubn;
+  A.ub_lock = D.ub_lock;
   A.cand = D.cand;
   A.cand_cap = D.cand_cap;
   A.cand_count = reinterpret_cast<unsigned long long*>(D.counters + 2);
@@ -609,16 +642,23 @@ int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stat
   A.ovf_list = D.ovf_list;
   A.ovf_count = D.counters + 1;
   A.progress = D.counters + 64;
-  auto screen = k == 1 ? k_dense_screen<true> : k_dense_screen<false>;
-  const int sms = ix->sms;
-  static std::atomic<uint32_t> attr_set{0};  // per (device, k == 1): smem attribute set once
-  const uint32_t bit = 1u << ((ix->device * 2 + (k == 1)) & 31);
-  if (!(attr_set.load() & bit)) {
-    SOFA_CK(cudaFuncSetAttribute(screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D_SMEM));
-    attr_set.fetch_or(bit);
+}
+
+int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stats, cudaStream_t st) {
+  DenseScratch& D = ix->dense;
+  int rc;
+  if (D.tmap_q_rows != q) {  // tensor maps are encoded once per buffer (not on every call)
+    if ((rc = make_tmap_bf16(reinterpret_cast<CUtensorMap*>(D.tmap_q), D.qb16, q, ix->len, ix->xb_ld, 16))) return rc;
+    if ((rc = make_tmap_bf16(reinterpret_cast<CUtensorMap*>(D.tmap_x), ix->xb16, ix->n, ix->len, ix->xb_ld, DM)))
+      return rc;
+    D.tmap_q_rows = q;
   }
-  screen<<<sms, D_THREADS, D_SMEM, st>>>(tmQ, tmX, A);
-  SOFA_LAUNCHED();
+  DenseArgs A{};
+  fill_screen_args(ix, k, A);
+  if ((rc = launch_screen(ix, *reinterpret_cast<const CUtensorMap*>(D.tmap_x),
+                          *reinterpret_cast<const CUtensorMap*>(D.tmap_q), A, dense_smem(ix->len, A.stages, A.nq_max),
+                          st)))
+    return rc;
 
   DensePost P{};
   P.series = ix->series;
@@ -649,7 +689,7 @@ int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stat
   P.oi = oi;
   P.dstats = stats ? ix->dstats : nullptr;
   const int nf4 = ix->len / 4;
-  const int grid = sms * 4;
+  const int grid = ix->sms * 4;
   if (nf4 <= 32)
     k_dense_post<1><<<grid, kThreads, 0, st>>>(P);
   else if (nf4 <= 64)
@@ -662,8 +702,58 @@ int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stat
   return SOFA_OK;
 }
 
+__global__ void k_to_bf16(const float* __restrict__ x, int64_t rows, int len, int ld, __nv_bfloat16* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows * ld; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / ld;
+    const int c = (int)(i % ld);
+    out[i] = __float2bfloat16_rn(c < len ? x[r * len + c] : 0.f);
+  }
+}
+
+// debug / verification entry (sofa_dense_dots): the screen's tensor-core dot products of bf16(rows)
+// and bf16(queries) (round to nearest), no screening, written as rows x q float32
+int dense_dots(const float* rows, int64_t m, int len, const float* queries, int q, float* out, cudaStream_t st) {
+  sofa_index tmp;
+  cudaGetDevice(&tmp.device);
+  cudaDeviceGetAttribute(&tmp.sms, cudaDevAttrMultiProcessorCount, tmp.device);
+  tmp.n = m;
+  tmp.len = len;
+  const int ld = (len + 7) / 8 * 8;
+  __nv_bfloat16 *xb = nullptr, *qb = nullptr;
+  int* prog = nullptr;
+  SOFA_CK(cudaMalloc(&xb, (size_t)m * ld * 2));
+  SOFA_CK(cudaMalloc(&qb, (size_t)q * ld * 2));
+  SOFA_CK(cudaMalloc(&prog, 1024 * 4));
+  SOFA_CK(cudaMemsetAsync(prog, 0, 1024 * 4, st));
+  k_to_bf16<<<1024, 256, 0, st>>>(rows, m, len, ld, xb);
+  k_to_bf16<<<256, 256, 0, st>>>(queries, q, len, ld, qb);
+  g_launches.fetch_add(2);
+  alignas(64) CUtensorMap ta, tb;
+  int rc = make_tmap_bf16(&ta, xb, m, len, ld, DM);
+  if (!rc) rc = make_tmap_bf16(&tb, qb, q, len, ld, 16);
+  if (!rc) {
+    DenseArgs A{};
+    A.n = m;
+    A.len = len;
+    A.k = 1;
+    A.KC = (len + DKC - 1) / DKC;
+    A.n_tiles = (m + DM - 1) / DM;
+    dense_geometry(len, A.stages, A.nq_max);
+    A.progress = prog;
+    A.raw_out = out;
+    A.raw_ld = q;
+    A.raw_q = q;
+    rc = launch_screen(&tmp, ta, tb, A, dense_smem(len, A.stages, A.nq_max), st);
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(xb);
+  cudaFree(qb);
+  cudaFree(prog);
+  return rc;
+}
+
 // scratch for q queries at k (grown on demand); counters: [0] dense slots, [1] overflow slots,
-// [2..3] candidate count (u64), [4] done CTAs.
+// [2..3] candidate count (u64), [4] done CTAs, [6..7] estimated refines; [64..] per-CTA progress.
 int ensure_dense_scratch(sofa_index* ix, int q, int k) {
   DenseScratch& D = ix->dense;
   if (D.q_cap >= q && D.k_cap >= k && D.len == ix->len) return SOFA_OK;
@@ -674,6 +764,7 @@ int ensure_dense_scratch(sofa_index* ix, int q, int k) {
   D.len = ix->len;
   D.cand_cap = ix->tune.dense_cand_cap > 0 ? ix->tune.dense_cand_cap : (int64_t)16 << 20;
   SOFA_CK(cudaMalloc(&D.qhat, (size_t)q * ix->len * 4));
+  SOFA_CK(cudaMalloc(&D.qb16, (size_t)q * ix->xb_ld * 2));
   SOFA_CK(cudaMalloc(&D.qparams, (size_t)q * 16));
   SOFA_CK(cudaMalloc(&D.qidx, (size_t)q * 4));
   SOFA_CK(cudaMalloc(&D.binit, (size_t)q * 4));
@@ -683,17 +774,20 @@ int ensure_dense_scratch(sofa_index* ix, int q, int k) {
   SOFA_CK(cudaMalloc(&D.tki, (size_t)q * k * 4));
   SOFA_CK(cudaMalloc(&D.tkn, (size_t)q * 4));
   SOFA_CK(cudaMalloc(&D.lock, (size_t)q * 4));
+  SOFA_CK(cudaMalloc(&D.ubl, (size_t)q * k * 4));
+  SOFA_CK(cudaMalloc(&D.ubn, (size_t)q * 4));
+  SOFA_CK(cudaMalloc(&D.ub_lock, (size_t)q * 4));
   SOFA_CK(cudaMalloc(&D.overflow, (size_t)q * 4));
   SOFA_CK(cudaMalloc(&D.ovf_list, (size_t)q * 4));
   SOFA_CK(cudaMalloc(&D.cand, (size_t)D.cand_cap * 8));
-  SOFA_CK(cudaMalloc(&D.counters, 64 + 1024 * 4));  // counters, then per-CTA progress
+  SOFA_CK(cudaMalloc(&D.counters, 64 * 4 + 1024 * 4));  // counters, then per-CTA progress
   return SOFA_OK;
 }
 
 void free_dense_scratch(sofa_index* ix) {
   DenseScratch& D = ix->dense;
-  void* ps[] = {D.qhat, D.qparams, D.qidx, D.binit, D.bsf, D.thr, D.tkd, D.tki, D.tkn, D.lock, D.overflow, D.ovf_list,
-                D.cand, D.counters};
+  void* ps[] = {D.qhat, D.qb16, D.qparams, D.qidx, D.binit, D.bsf, D.thr, D.tkd, D.tki, D.tkn, D.lock, D.ubl,
+                D.ubn, D.ub_lock, D.overflow, D.ovf_list, D.cand, D.counters};
   for (void* p : ps)
     if (p) cudaFree(p);
   D = DenseScratch{};

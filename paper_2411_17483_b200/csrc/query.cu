@@ -115,6 +115,9 @@ struct QArgs {
   int* counters;       // [2s] ranks used in set s, [2s+1] its cursor
   int* qd_counter;
   float* d_qhat;
+  __nv_bfloat16* d_qb16;
+  int xb_ld;
+  int *d_ubn, *d_ublock;
   float4* d_qparams;
   int* d_qidx;
   float *d_binit, *d_bsf, *d_thr, *d_tkd;
@@ -1114,32 +1117,38 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
       if (s_dense >= 0) {
         // publish the query's state to its dense slot; dense.cu finishes it
         const int slot = s_dense;
-        for (int t = tid; t < len; t += kQThreads) A.d_qhat[(int64_t)slot * len + t] = reinterpret_cast<const float*>(s_qh4)[t];
+        for (int t = tid; t < len; t += kQThreads) {
+          const float v = reinterpret_cast<const float*>(s_qh4)[t];
+          A.d_qhat[(int64_t)slot * len + t] = v;
+          A.d_qb16[(int64_t)slot * A.xb_ld + t] = __float2bfloat16_rn(v);  // the screen's operand
+        }
         for (int r = tid; r < S.tkn; r += kQThreads) {
           A.d_tkd[(int64_t)slot * A.k + r] = s_tkd[r];
           A.d_tki[(int64_t)slot * A.k + r] = s_tki[r];
         }
         if (warp == 0) {
-          double nq = 0.0, sq = 0.0;
+          double nq = 0.0;
           for (int t = lane; t < len; t += 32) {
             const double v = reinterpret_cast<const float*>(s_qh4)[t];
             nq += v * v;
-            sq += v;
           }
           nq = warp_sum_f64(nq);
-          sq = warp_sum_f64(sq);
           if (lane == 0) {
-            // TF32 operands keep 10 mantissa bits: |dot error| <= gamma sum|q x|, gamma = 2^-9 (two
-            // truncated operands) + len 2^-22 (fp32 accumulation, doubled for safety), +5%
-            const double gamma = 1.05 * 0x1p-9 + (double)len * 0x1p-22;
-            A.d_qparams[slot] = make_float4((float)nq, (float)sq, (float)(2.0 * gamma * sqrt(nq) * 1.0001),
-                                            (float)(2e-4 * nq + 1e-3));
+            // bf16 operands round to nearest (relative error <= 2^-8 each), products are exact, the
+            // fp32 accumulation is bounded as a naive sum (K 2^-24) and doubled: |dot error| <=
+            // gamma |x^| |q^| with |x^| <= sqrt(1.0001 n); plus slack for |x^|^2 = n (float32
+            // statistics) and the refine's own float32 rounding (dense.cu header, DESIGN reading 29)
+            const double gamma = 0x1p-7 + 0x1p-15 + (double)len * 0x1p-23;
+            const double eps = 2.0 * gamma * sqrt(1.0001 * len) * sqrt(nq) + 2e-4 * (nq + len) + 1e-3;
+            A.d_qparams[slot] = make_float4((float)nq, (float)eps, 0.f, 0.f);
             A.d_qidx[slot] = qi;
             A.d_binit[slot] = S.bsf_init;
             A.d_bsf[slot] = S.bsf;
-            A.d_thr[slot] = S.bsf;
+            A.d_thr[slot] = S.tkn == A.k ? S.bsf : S.bsf_init;  // proven bound on the k-th best (or +inf)
             A.d_tkn[slot] = S.tkn;
             A.d_lock[slot] = 0;
+            A.d_ubn[slot] = 0;
+            A.d_ublock[slot] = 0;
             A.d_overflow[slot] = 0;
           }
         }
@@ -1389,7 +1398,7 @@ int launch_query_impl(sofa_index* ix, const float* Q, int q, int k, const float*
   A.qcounter = ix->qcounter;
   A.dstats = ix->dstats;
   A.trace = ix->trace_on ? ix->trace + ix->trace_off * SOFA_TRACE_FIELDS : nullptr;
-  if (ix->dense_permille > 0 && ix->dense.q_cap >= q) {
+  if (ix->dense_permille > 0 && ix->xb16 && ix->dense.q_cap >= q) {
     const DenseScratch& D = ix->dense;
     A.dense_min = (ix->nb * (ix->dense_permille < 1000 ? ix->dense_permille : 0) + 999) / 1000;
     if (A.dense_min < 1) A.dense_min = 1;
@@ -1397,6 +1406,10 @@ int launch_query_impl(sofa_index* ix, const float* Q, int q, int k, const float*
     A.dense_force = ix->dense_permille >= 1000;
     A.qd_counter = D.counters;
     A.d_qhat = D.qhat;
+    A.d_qb16 = D.qb16;
+    A.xb_ld = ix->xb_ld;
+    A.d_ubn = D.ubn;
+    A.d_ublock = D.ub_lock;
     A.d_qparams = D.qparams;
     A.d_qidx = D.qidx;
     A.d_binit = D.binit;

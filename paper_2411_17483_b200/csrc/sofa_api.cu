@@ -224,7 +224,7 @@ void sofa_free(sofa_index* ix) {
   for (auto* v : {&ix->ktime_pending, &ix->ktime_free})
     for (auto& quad : *v)
       for (auto e : quad) cudaEventDestroy(e);
-  void* bufs[] = {ix->qstate, ix->q_T, ix->q_hat, ix->pool, ix->tasks, ix->rank_count, ix->words, ix->stats, ix->stats_orig, ix->perm, ix->env, ix->bkey, ix->basis32, ix->basis64, ix->edges32,
+  void* bufs[] = {ix->qstate, ix->q_T, ix->q_hat, ix->pool, ix->tasks, ix->rank_count, ix->words, ix->stats, ix->stats_orig, ix->perm, ix->env, ix->bkey, ix->xb16, ix->basis32, ix->basis64, ix->edges32,
                   ix->edges64, ix->gscratch, ix->qcounter, ix->dstats, ix->hq_dev, ix->hd_dev, ix->hi_dev,
                   ix->trace};
   for (void* p : bufs)
@@ -365,7 +365,18 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
   const int64_t env_nodes = ix->lvl_off[ix->nlev - 1] + ix->lvl_cnt[ix->nlev - 1];
   BCK(cudaMalloc(&ix->env, (size_t)env_nodes * 2 * WS));
   BCK(cudaMalloc(&ix->bkey, (size_t)ix->nb * 8));
-  if ((rc = launch_transform(series_dev, n, ix->dm, ix->model, words_u, stats_u, keys_u, nullptr, nullptr, nullptr, st))) {
+  // the dense screen's operand (f1): the z-normalised rows in bfloat16, written by the same pass; if the
+  // device cannot hold it the index runs without the dense path (same results, sparse only)
+  ix->xb_ld = (len + 7) / 8 * 8;
+  if (ix->dense_permille > 0) {
+    if (cudaMalloc(&ix->xb16, (size_t)n * ix->xb_ld * 2) != cudaSuccess) {
+      cudaGetLastError();
+      ix->xb16 = nullptr;
+      ix->dense_permille = 0;
+    }
+  }
+  if ((rc = launch_transform(series_dev, n, ix->dm, ix->model, words_u, stats_u, keys_u, nullptr, nullptr, ix->xb16,
+                             st))) {
     freeall();
     return bail(rc);
   }
@@ -422,7 +433,7 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
   }
   if (stats) ix->trace_q = q;
   int rc;
-  const bool dense = ix->n > 0 && ix->dense_permille > 0;
+  const bool dense = ix->n > 0 && ix->dense_permille > 0 && ix->xb16;
   // large batches run as consecutive sub-batches of kQueryBatch queries on the same stream (the scan
   // pool holds one leaf list per query: q x ceil(n/B) entries)
   const int qb_max = q < kQueryBatch ? q : kQueryBatch;
@@ -452,7 +463,7 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
     float* Db = out_dist_dev + (int64_t)q0 * k;
     int64_t* Ib = out_idx_dev + (int64_t)q0 * k;
     ix->trace_off = q0;
-    if (dense) SOFA_CK(cudaMemsetAsync(ix->dense.counters, 0, 64 + 1024 * 4, st));
+    if (dense) SOFA_CK(cudaMemsetAsync(ix->dense.counters, 0, (64 + 1024) * 4, st));
     if (rec) cudaEventRecord(ev[0], st);
     if (ix->n == 0) {
       rc = launch_fill_pad(Db, Ib, (int64_t)qb * k, st);
@@ -613,6 +624,15 @@ int sofa_transform(const float* series_dev, int64_t n, const sofa_model* model, 
   return rc;
 }
 
+int sofa_dense_dots(const float* rows_dev, int64_t m, int32_t len, const float* queries_dev, int32_t q,
+                    float* out_dev, void* cuda_stream) {
+  g_err.clear();
+  if (!rows_dev || !queries_dev || !out_dev) return fail(SOFA_EINVAL, "NULL pointer");
+  if (m < 1 || q < 1 || q > 256) return fail(SOFA_EINVAL, "need m >= 1 and 1 <= q <= 256");
+  if (len < 4 || len > SOFA_MAX_LEN || len % 4) return fail(SOFA_EINVAL, "len must be a multiple of 4 in [4, 1024]");
+  return dense_dots(rows_dev, m, len, queries_dev, q, out_dev, (cudaStream_t)cuda_stream);
+}
+
 int sofa_get_info(const sofa_index* ix, sofa_index_info* out) {
   if (!ix || !out) return fail(SOFA_EINVAL, "NULL pointer");
   out->n = ix->n;
@@ -625,6 +645,7 @@ int sofa_get_info(const sofa_index* ix, sofa_index_info* out) {
   out->block_size = ix->B;
   out->word_stride = ix->WS;
   for (int i = 0; i < 4; ++i) out->build_ms[i] = ix->build_ms[i];
+  out->dense_enabled = ix->dense_permille > 0 && ix->xb16 != nullptr;
   return SOFA_OK;
 }
 

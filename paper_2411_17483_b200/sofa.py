@@ -78,7 +78,7 @@ class sofa_knn_stats(C.Structure):
 class sofa_index_info(C.Structure):
     _fields_ = [("n", C.c_int64), ("n_blocks", C.c_int64), ("global_offset", C.c_int64), ("global_n", C.c_int64),
                 ("len", C.c_int32), ("l", C.c_int32), ("alphabet", C.c_int32), ("block_size", C.c_int32),
-                ("word_stride", C.c_int32), ("build_ms", C.c_double * 4)]
+                ("word_stride", C.c_int32), ("build_ms", C.c_double * 4), ("dense_enabled", C.c_int32)]
 
 
 _LIB = None
@@ -111,6 +111,7 @@ def lib() -> C.CDLL:
         L.sofa_transform.argtypes = [VP, I64, P(sofa_model), VP, VP, VP]
         L.sofa_get_info.argtypes = [VP, P(sofa_index_info)]
         L.sofa_export_index.argtypes = [VP, VP, VP, VP, VP, VP]
+        L.sofa_dense_dots.argtypes = [VP, I64, I32, VP, I32, VP, VP]
         L.sofa_free.argtypes = [VP]
         L.sofa_free.restype = None
         _LIB = L
@@ -240,6 +241,10 @@ def sofa_get_info(ix) -> sofa_index_info:
 def sofa_export_index(ix, words_sorted_dev=None, perm_dev=None, env_dev=None, block_keys_dev=None, stream=None):
     _ck(lib().sofa_export_index(ix, _ptr(words_sorted_dev), _ptr(perm_dev), _ptr(env_dev), _ptr(block_keys_dev),
                                 _stream(stream)))
+
+
+def sofa_dense_dots(rows_dev, m, len_, queries_dev, q, out_dev, stream=None):
+    _ck(lib().sofa_dense_dots(_ptr(rows_dev), m, len_, _ptr(queries_dev), q, _ptr(out_dev), _stream(stream)))
 
 
 def sofa_free(ix):

@@ -114,3 +114,39 @@ def test_batch_decision_defers_few_flagged_queries():
     ix, d, i, st = _check(x, q, 1, sample_size=datagen.default_sample_size(w))
     assert st["dense_queries"] == 0
     assert np.array_equal(i[:, 0].cpu().numpy(), datagen.query_sources(w))
+
+
+@pytest.mark.parametrize("n,q,m", [(256, 200, 4096 + 77), (1024, 64, 1500), (100, 37, 999), (256, 256, 300)])
+def test_dense_dots_within_bound(n, q, m):
+    """the tensor cores' own accumulation (tcgen05.mma kind::f16, read back raw through
+    sofa_dense_dots) against the bound the screen assumes: products of the bf16 operands
+    exact, fp32 accumulation error <= n 2^-23 sum|x_t q_t|; and the total error against the float32
+    inputs <= gamma |x| |q| (gamma = 2^-7 + 2^-15 + n 2^-23).  Adversarial rows: alternating large
+    values that cancel, values on bf16 rounding midpoints, z-normalised walks, zeros"""
+    from paper_2411_17483_b200 import sofa as S
+    from test_dense_bound import bf16
+    rng = np.random.default_rng(n * 7 + q)
+    x = np.cumsum(rng.normal(size=(m, n)), axis=1)
+    x = ((x - x.mean(1, keepdims=True)) / x.std(1, keepdims=True)).astype(np.float32)
+    alt = np.where(np.arange(n) % 2 == 0, 1.0, -1.0)
+    x[:40] = (alt[None, :] * rng.uniform(1, 30, size=(40, 1)) + rng.normal(scale=1e-3, size=(40, n))).astype(np.float32)
+    mid = (1.0 + (2 * rng.integers(0, 128, size=(40, n)) + 1) * 2.0 ** -8).astype(np.float32)  # bf16 ties
+    x[40:80] = mid * rng.choice([-1.0, 1.0], size=(40, n))
+    x[80:90] = 0.0
+    qs = rng.normal(size=(q, n)).astype(np.float32)
+    qs[0] = 1.0                       # against the alternating rows: heavy cancellation
+    qs[1] = alt.astype(np.float32)    # ... or none
+    xd, qd = torch.from_numpy(x).cuda(), torch.from_numpy(qs).cuda()
+    out = torch.empty(m, q, dtype=torch.float32, device="cuda")
+    S.sofa_dense_dots(xd, m, n, qd, q, out)
+    hw = out.cpu().numpy().astype(np.float64)
+    xb, qb = bf16(x).astype(np.float64), bf16(qs).astype(np.float64)
+    exact = xb @ qb.T
+    absprod = np.abs(xb) @ np.abs(qb).T
+    acc_err = np.abs(hw - exact)
+    assert np.all(acc_err <= n * 2.0 ** -23 * absprod), (acc_err / np.maximum(absprod, 1e-30)).max()
+    gamma = 2.0 ** -7 + 2.0 ** -15 + n * 2.0 ** -23
+    tot = np.abs(hw - x.astype(np.float64) @ qs.astype(np.float64).T)
+    bound = gamma * np.linalg.norm(x.astype(np.float64), axis=1)[:, None] * np.linalg.norm(qs.astype(np.float64), axis=1)[None, :]
+    assert np.all(tot <= bound + 1e-30), (tot / np.maximum(bound, 1e-30)).max()
+    assert np.all(hw[80:90] == 0.0)
