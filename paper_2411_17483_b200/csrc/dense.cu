@@ -46,8 +46,10 @@ constexpr int DM = 128;                  // rows per tile (MMA M = TMEM lanes)
 constexpr int DKC = 64;                  // bf16 per K chunk = 128-byte rows (SWIZZLE_128B atom)
 constexpr int DA_BYTES = DM * DKC * 2;   // 16 KB per A stage
 constexpr int D_THREADS = 320;           // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2..9 epilogue
-constexpr int D_AHEAD = 3;               // row tiles a CTA may run ahead of its twins
-constexpr int D_SMEM_MAX = 232448;       // opt-in shared memory per CTA on sm_100
+constexpr int D_AHEAD = 8;               // row tiles a CTA may run ahead of its twins
+constexpr int D_MAX_STAGES = 8;          // A ring depth cap (barrier arrays)
+constexpr int D_REFRESH = 16;            // tiles between re-reads of the other CTAs' thresholds
+constexpr int D_SMEM_MAX = 232448 - 2048;  // opt-in shared memory per CTA on sm_100, less the static part
 constexpr int D_MISC = 4096;             // per-query thresholds / norms + barriers
 
 // ------------------------------------------------------------------------------- PTX helpers
@@ -118,7 +120,7 @@ struct DenseArgs {
   int len, k, KC;
   int64_t n_tiles;
   int nq_max;                // queries per group (shared memory / TMEM limit of this launch)
-  int stages;                // A ring depth
+  int smem_dyn;              // dynamic shared memory of the launch (the A ring takes what the queries leave)
   const float2* stats_orig;  // (mu, inv_sigma) per original row
   const int* qd_count;       // number of dense query slots (device)
   const float4* qparams;     // per slot: (|q^|^2, eps, -, -)
@@ -220,9 +222,11 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   if (b >= cpg * ng) return;                                   // (only with more groups than CTAs / group)
   const int grp = b % ng, twin = b / ng;
   const int q0 = grp * nq, nqv = qd - q0 < nq ? qd - q0 : nq;  // valid columns of this group
-  const int S = A.stages, KC = A.KC;
+  const int KC = A.KC;
+  int S = (A.smem_dyn - 1024 - KC * nq * 128 - D_MISC) / DA_BYTES;  // as deep as the queries leave room for
+  S = S > D_MAX_STAGES ? D_MAX_STAGES : S;
   unsigned char* sB = dsm;                                     // KC x nq x 128 B (resident)
-  unsigned char* sA = dsm + (size_t)KC * A.nq_max * 128;       // S x 16 KB
+  unsigned char* sA = dsm + (size_t)KC * nq * 128;             // S x 16 KB
   float* s_d = reinterpret_cast<float*>(sA + (size_t)S * DA_BYTES);  // nq: thr + eps - |q^|^2
   float* s_qn = s_d + 256;                                            // nq: |q^|^2
   float* s_eps = s_qn + 256;                                          // nq: eps
@@ -275,19 +279,21 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       // the group's queries: every K chunk, 16 rows per box, resident for the whole pass
       mbar_expect_tx(bfull, (uint32_t)(KC * nq * 128));
       for (int kc = 0; kc < KC; ++kc)
-        for (int r = 0; r < nq; r += 16) tma_load_2d(sB + ((size_t)kc * A.nq_max + r) * 128, &tmB, kc * DKC, q0 + r, bfull);
+        for (int r = 0; r < nq; r += 16) tma_load_2d(sB + ((size_t)kc * nq + r) * 128, &tmB, kc * DKC, q0 + r, bfull);
       volatile int* prog = A.progress;
       int stage = 0;
       uint32_t phase = 0;
       int64_t j = 0;
+      int twin_lo = 0;  // the slowest twin's progress, re-read only when this CTA would run too far ahead
       for (int64_t t = twin; t < T; t += cpg, ++j) {
-        if (ng > 1) {  // stay within D_AHEAD tiles of the twins (the tile is then still in L2 for them)
-          for (;;) {
+        if (ng > 1 && twin_lo < j - D_AHEAD) {  // stay within D_AHEAD tiles of the twins (the tile is still
+          for (;;) {                            // in L2 when they read it)
             int lo = 0x7fffffff;
             for (int o = 0; o < ng; ++o) {
               const int p = prog[twin * ng + o];
               lo = p < lo ? p : lo;
             }
+            twin_lo = lo;
             if (lo >= j - D_AHEAD) break;
             __nanosleep(256);
           }
@@ -324,7 +330,7 @@ __global__ void __launch_bounds__(D_THREADS, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * DA_BYTES);
-          const uint32_t b0 = smem_u32(sB + (size_t)kc * A.nq_max * 128);
+          const uint32_t b0 = smem_u32(sB + (size_t)kc * nq * 128);
 #pragma unroll
           for (int kk = 0; kk < DKC / 16; ++kk)  // UMMA_K = 16 bf16 = 32 bytes along the swizzled row
             tc_mma_bf16(dt, sdesc_sw128(a0 + 32 * kk), sdesc_sw128(b0 + 32 * kk), idesc, (kc | kk) ? 1u : 0u);
@@ -347,12 +353,18 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     const int nch = nq / 16;
     const float nlen = (float)A.len;
     int64_t j = 0;
+    auto xnorm = [&](int64_t tt) {  // |x^|^2 of this thread's row of tile tt: n, 0 for a constant row, NaN past N
+      const int64_t rr = tt * DM + r;
+      if (rr >= A.n || tt >= T) return __int_as_float(0x7fffffff);
+      return A.stats_orig[rr].y > 0.f ? nlen : 0.f;
+    };
+    float xn_next = xnorm(twin);
     for (int64_t t = twin; t < T; t += cpg, ++j) {
       const int acc = (int)(j & 1);
       const uint32_t aph = (uint32_t)((j >> 1) & 1);
       const int64_t row = t * DM + r;
-      float xn = __int_as_float(0x7fffffff);  // past the last row: NaN, never a candidate
-      if (row < A.n) xn = A.stats_orig[row].y > 0.f ? nlen : 0.f;
+      const float xn = xn_next;  // loaded one tile ahead
+      xn_next = xnorm(t + cpg);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(qtr * 32) << 16) + (uint32_t)(acc * 256);
@@ -395,8 +407,8 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      // other CTAs' improvements of the thresholds (global) into this CTA's copy
-      if (qtr == 0 && !A.raw_out)
+      // other CTAs' improvements of the thresholds (global) into this CTA's copy, now and then
+      if (qtr == 0 && !A.raw_out && (j % D_REFRESH) == D_REFRESH - 1)
         for (int c = lane + 32 * half; c < nqv; c += 64) {
           const float nd = *(volatile float*)&A.thr[q0 + c] + s_eps[c] - s_qn[c];
           if (nd < s_d[c]) smem_fmin(s_d + c, nd);
@@ -572,27 +584,14 @@ static int make_tmap_bf16(CUtensorMap* m, const __nv_bfloat16* base, int64_t row
   return SOFA_OK;
 }
 
-// launch geometry of the screen for row length `len`: A ring depth and the queries per group that fit
-// next to it (multiple of 16, <= 256 for the 2 x 256 TMEM accumulator columns)
-static void dense_geometry(int len, int& stages, int& nq_max) {
+// launch geometry of the screen for row length `len`: the queries per group that fit next to an A ring
+// of at least 4 stages (multiple of 16, <= 256 for the 2 x 256 TMEM accumulator columns); the kernel
+// then deepens the ring into whatever its group's queries leave free (up to D_MAX_STAGES)
+static void dense_geometry(int len, int& nq_max) {
   const int KC = (len + DKC - 1) / DKC;
-  nq_max = 0;
-  stages = 4;
-  for (int s = 4; s >= 2; --s) {
-    const int avail = D_SMEM_MAX - 1024 - s * DA_BYTES - D_MISC;
-    int nq = avail / (KC * 128) / 16 * 16;
-    if (nq > 256) nq = 256;
-    if (nq > nq_max) {
-      nq_max = nq;
-      stages = s;
-    }
-    if (nq >= 256) break;
-  }
-}
-
-static size_t dense_smem(int len, int stages, int nq_max) {
-  const int KC = (len + DKC - 1) / DKC;
-  return 1024 + (size_t)KC * nq_max * 128 + (size_t)stages * DA_BYTES + D_MISC;
+  const int avail = D_SMEM_MAX - 1024 - 4 * DA_BYTES - D_MISC;
+  const int nq = avail / (KC * 128) / 16 * 16;
+  nq_max = nq > 256 ? 256 : nq;
 }
 
 static int launch_screen(sofa_index* ix, const CUtensorMap& tmA, const CUtensorMap& tmB, const DenseArgs& A,
@@ -627,7 +626,8 @@ static void fill_screen_args(sofa_index* ix, int k, DenseArgs& A) {
   A.k = k;
   A.KC = (ix->len + DKC - 1) / DKC;
   A.n_tiles = (ix->n + DM - 1) / DM;
-  dense_geometry(ix->len, A.stages, A.nq_max);
+  dense_geometry(ix->len, A.nq_max);
+  A.smem_dyn = D_SMEM_MAX;
   A.stats_orig = ix->stats_orig;
   A.qd_count = D.counters;
   A.qparams = D.qparams;
@@ -656,7 +656,7 @@ int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stat
   DenseArgs A{};
   fill_screen_args(ix, k, A);
   if ((rc = launch_screen(ix, *reinterpret_cast<const CUtensorMap*>(D.tmap_x),
-                          *reinterpret_cast<const CUtensorMap*>(D.tmap_q), A, dense_smem(ix->len, A.stages, A.nq_max),
+                          *reinterpret_cast<const CUtensorMap*>(D.tmap_q), A, D_SMEM_MAX,
                           st)))
     return rc;
 
@@ -738,12 +738,13 @@ int dense_dots(const float* rows, int64_t m, int len, const float* queries, int 
     A.k = 1;
     A.KC = (len + DKC - 1) / DKC;
     A.n_tiles = (m + DM - 1) / DM;
-    dense_geometry(len, A.stages, A.nq_max);
+    dense_geometry(len, A.nq_max);
+    A.smem_dyn = D_SMEM_MAX;
     A.progress = prog;
     A.raw_out = out;
     A.raw_ld = q;
     A.raw_q = q;
-    rc = launch_screen(&tmp, ta, tb, A, dense_smem(len, A.stages, A.nq_max), st);
+    rc = launch_screen(&tmp, ta, tb, A, D_SMEM_MAX, st);
   }
   cudaStreamSynchronize(st);
   cudaFree(xb);

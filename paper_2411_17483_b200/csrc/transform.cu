@@ -68,7 +68,8 @@ struct TransformArgs {
   uint64_t* keys;
   double* vals;
   uint8_t* words_l;
-  __nv_bfloat16* xb16;          // nullable: N x len z-normalised rows (dense screen operand)
+  __nv_bfloat16* xb16;          // nullable: N x xb_ld z-normalised rows (dense screen operand)
+  int xb_ld;
 };
 
 // 2 CTAs (16 warps, up to 128 registers) when the fold or wide words need the registers, else 3
@@ -128,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, (FOLD || LT > 16) ? 2 : 3) k_transfo
           uint2 pk;
           pk.x = *reinterpret_cast<uint32_t*>(&lo);
           pk.y = *reinterpret_cast<uint32_t*>(&hi);
-          *reinterpret_cast<uint2*>(A.xb16 + row * len + 4 * fi) = pk;
+          *reinterpret_cast<uint2*>(A.xb16 + row * A.xb_ld + 4 * fi) = pk;
         }
       }
     }
@@ -364,6 +365,7 @@ int launch_transform(const float* X, int64_t N, const DevModel& dm, const sofa_m
   A.vals = vals;
   A.words_l = words_l;
   A.xb16 = xb16;
+  A.xb_ld = (dm.len + 7) / 8 * 8;
 #define SOFA_TR(g, lt)                                                                        \
   if (G == g && dm.LT == lt)                                                                  \
     return fold ? launch_transform_t<g, lt, true>(A, dm, m, st) : launch_transform_t<g, lt, false>(A, dm, m, st);
