@@ -108,12 +108,15 @@ __device__ __forceinline__ uint32_t idesc_bf16(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(DM >> 4) << 24);
 }
 
-#define TMEM_LD16(addr, r)                                                                                 \
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),   \
-                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),          \
-                 "=r"(r[15])                                                                                       \
-               : "r"(addr))
+#define TMEM_LD32(addr, r)                                                                                        \
+  asm volatile(                                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19," \
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                                   \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),           \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),     \
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),   \
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])    \
+      : "r"(addr))
 
 struct DenseArgs {
   int64_t n, dense_rows;
@@ -350,12 +353,13 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     // for that query iff val >= |x^|^2 (LB_g <= thr).
     const int qtr = warp & 3, half = (warp - 2) >> 2;
     const int r = qtr * 32 + lane;
-    const int nch = nq / 16;
+    const int nch = (nq + 31) / 32;  // 32-column chunks (columns past the group's queries have s_d = -inf)
     const float nlen = (float)A.len;
     int64_t j = 0;
     auto xnorm = [&](int64_t tt) {  // |x^|^2 of this thread's row of tile tt: n, 0 for a constant row, NaN past N
       const int64_t rr = tt * DM + r;
       if (rr >= A.n || tt >= T) return __int_as_float(0x7fffffff);
+      if (A.raw_out) return 0.f;
       return A.stats_orig[rr].y > 0.f ? nlen : 0.f;
     };
     float xn_next = xnorm(twin);
@@ -368,42 +372,54 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(qtr * 32) << 16) + (uint32_t)(acc * 256);
-      for (int ch = half; ch < nch; ch += 2) {
-        uint32_t v[16];
-        TMEM_LD16(tbase + ch * 16, v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        const int c0 = ch * 16;
+      // screen 32 columns held in v (registers): val = 2 dot + (thr + eps - |q^|^2) >= |x^|^2 ?
+      auto screen = [&](const uint32_t (&v)[32], int c0) {
         if (A.raw_out) {
           if (row < A.n)
-            for (int c = 0; c < 16; ++c)
+            for (int c = 0; c < 32; ++c)
               if (c0 + c < nqv) A.raw_out[row * A.raw_ld + q0 + c0 + c] = __uint_as_float(v[c]);
-          continue;
+          return;
         }
         float vmax = -INFINITY;
-        float val[16];
 #pragma unroll
-        for (int c = 0; c < 16; c += 4) {
+        for (int c = 0; c < 32; c += 4) {
           const float4 d4 = *reinterpret_cast<const float4*>(s_d + c0 + c);
-          val[c + 0] = fmaf(2.f, __uint_as_float(v[c + 0]), d4.x);
-          val[c + 1] = fmaf(2.f, __uint_as_float(v[c + 1]), d4.y);
-          val[c + 2] = fmaf(2.f, __uint_as_float(v[c + 2]), d4.z);
-          val[c + 3] = fmaf(2.f, __uint_as_float(v[c + 3]), d4.w);
-          vmax = fmaxf(vmax, fmaxf(fmaxf(val[c], val[c + 1]), fmaxf(val[c + 2], val[c + 3])));
+          const float a0 = fmaf(2.f, __uint_as_float(v[c + 0]), d4.x);
+          const float a1 = fmaf(2.f, __uint_as_float(v[c + 1]), d4.y);
+          const float a2 = fmaf(2.f, __uint_as_float(v[c + 2]), d4.z);
+          const float a3 = fmaf(2.f, __uint_as_float(v[c + 3]), d4.w);
+          vmax = fmaxf(vmax, fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)));
         }
         if (__any_sync(FULL, vmax >= xn)) {  // rare: this chunk has candidates
+#pragma unroll 1
+          for (int c = 0; c < 32; ++c) {
+            float dot = 0.f;
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const bool pass = val[c] >= xn;
-            if (!__any_sync(FULL, pass)) continue;
+            for (int u = 0; u < 32; ++u)  // select without dynamic register indexing
+              if (u == c) dot = __uint_as_float(v[u]);
             const int col = c0 + c;
+            const bool pass = fmaf(2.f, dot, s_d[col]) >= xn;
+            if (!__any_sync(FULL, pass)) continue;
             emit_candidate(A, pass, q0 + col, (uint32_t)row);
             if (pass) {
-              const float dot = __uint_as_float(v[c]);
               const float ub = (s_qn[col] + xn - 2.f * dot) + s_eps[col];
               offer_ub(A, q0 + col, ub, s_d + col, s_eps[col] - s_qn[col]);
             }
           }
         }
+      };
+      // TMEM loads double-buffered: the next chunk is in flight while this one is screened
+      uint32_t va[32], vb[32];
+      if (half < nch) TMEM_LD32(tbase + half * 32, va);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int ch = half; ch < nch; ch += 4) {
+        if (ch + 2 < nch) TMEM_LD32(tbase + (ch + 2) * 32, vb);
+        screen(va, ch * 32);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (ch + 2 >= nch) break;
+        if (ch + 4 < nch) TMEM_LD32(tbase + (ch + 4) * 32, va);
+        screen(vb, (ch + 2) * 32);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
