@@ -92,6 +92,17 @@ def dense_roofline(st, km, rows, w, bf16, bf16_kind):
     return dn
 
 
+def build_report(index, build_ms, rows, w):
+    """build (a1-a4) time and its phases (sofa_get_info.build_ms, CUDA events on the build stream); the
+    transform (a1 + a3) reads the rows once and writes words, statistics and the bf16 row copy"""
+    ph = index.info["build_ms"]
+    series = rows * w.length * 4
+    written = rows * (16 * ((w.l + 15) // 16) + 8 + 8 + 2 * w.length)
+    return {"ms": build_ms, "gb_per_s_series_read": series / (build_ms / 1e3) / 1e9, "phases_ms": ph,
+            "transform_gb_per_s": (series + written) / (ph["transform"] / 1e3) / 1e9 if ph["transform"] > 0 else None,
+            "transform_bytes": series + written}
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -122,11 +133,14 @@ class Clocks:
 
     def __init__(self, dev: int):
         self.dev, self.rows, self.proc = dev, [], None
+        self.period_ms = int(os.environ.get("SOFA_BENCH_SMI_MS", "100"))
 
     def __enter__(self):
         try:
+            if self.period_ms <= 0:  # diagnostic only (SOFA_BENCH_SMI_MS=0): no clock record
+                return self
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-i", str(self.dev), "-lms", "100"], stdout=subprocess.PIPE,
+                                          "-i", str(self.dev), "-lms", str(self.period_ms)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -304,6 +318,7 @@ def main():
 
     # ---------------------------------------------------------------- timed steps
     times = []
+    km_steps = []
     launches0 = S.sofa_launch_count()
     index.kernel_timing(1)  # per-kernel-group CUDA events inside every timed step (no sync)
     with Clocks(local) as clk:
@@ -319,8 +334,11 @@ def main():
             torch.cuda.synchronize()
             barrier()
             times.append(s0.elapsed_time(s1))
+            km_step, _ = index.kernel_timing(1)  # this step's groups (after the sync; restarts the totals)
+            km_steps.append(km_step)
         launches = S.sofa_launch_count() - launches0
-        km_tot, km_groups = index.kernel_timing(0)
+        index.kernel_timing(0)
+        km_tot = {kk: sum(m[kk] for m in km_steps) for kk in km_steps[0]}
         # keep sampling clocks for a short sustained run of the same step (no timing taken)
         t_end = time.time() + 1.0
         while time.time() < t_end:
@@ -445,8 +463,9 @@ def main():
                       "refined_per_query": st["refined"] / st["queries"],
                       "words_scanned_per_query": st["words_scanned"] / st["queries"]},
             "knn_stats": st,
-            "build": {"ms": build_ms, "gb_per_s_series_read": (hi - lo) * w.length * 4 / (build_ms / 1e3) / 1e9},
-            "roofline": roofline, "roofline_all": rooflines, "kernel_ms": km,
+            "build": build_report(index, build_ms, hi - lo, w),
+            "roofline": roofline, "roofline_all": rooflines, "kernel_ms": km, "step_ms": [round(t, 4) for t in times],
+            "kernel_ms_steps": {kk: [round(m[kk], 4) for m in km_steps] for kk in km},
             "cpu_baseline": cpu, "cpu_scan": cpu_scan_line, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)

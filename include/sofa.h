@@ -82,14 +82,16 @@ typedef struct {
   int32_t block_size;      /* B series per leaf block, default 256 (reading 19) */
   int32_t candidate_limit; /* max complex index eligible for selection; 0 => n/2 (reading 3) */
   int32_t binning;         /* SOFA_BINNING_EQUI_DEPTH (default), _EQUI_WIDTH or _ISAX */
-  int32_t dense_permille;  /* dense path for a query whose leaf list still keeps
-                              >= this many permille of the blocks after its 8 lowest-LB leaves
-                              were refined and >= 1/16 of their words still pass the tightened
-                              bound; the batch runs the tensor-core pass only if the flagged
-                              queries' estimated refines add up to one pass over the rows (else a
-                              second sparse launch finishes them).  0 => 100 (10%), < 0 => never,
-                              >= 1000 => every query with a surviving leaf (testing).  Results are
-                              identical either way; only speed changes. */
+  int32_t dense_permille;  /* dense path: a strided probe of 2048 stored words
+                              estimates the fraction of rows the sparse path would refine.  A query
+                              is flagged before its envelope-tree descent if >= 10% of the probe
+                              passes the bound of its own-key seed, else after top-M seeding if >=
+                              this many permille pass the tightened bound (and the estimate is >=
+                              4096 rows either way).  The batch runs the tensor-core pass only if
+                              the flagged queries' estimated refines add up to one pass over the
+                              rows (sofa_tuning.dense_batch_rows); else the scan pool finishes them
+                              sparsely.  0 => 20 (2%), < 0 => never, >= 1000 => every query
+                              (testing).  Results are identical either way; only speed changes. */
   int64_t global_offset;   /* global index of this shard's row 0 (0 on one GPU) */
   int64_t global_n;        /* total rows over all shards (0 => this call's n) */
   const sofa_model* model; /* nullable: NULL => learn from this call's rows at the global
@@ -140,6 +142,13 @@ typedef struct {
   int32_t scan_wide;       /* the same for the scan pool */
   int64_t dense_cand_cap;  /* dense-path candidate buffer entries (0 => 16M); a query whose candidates
                               overflow it is rescanned brute force (testing) */
+  int64_t dense_batch_rows; /* the batch runs the dense pass iff its flagged queries' estimated sparse
+                              refines add up to at least this many rows (0 => n, one pass over the
+                              rows); a batch below it scans its flagged queries sparsely */
+  int32_t dense_diag;      /* TIMING DIAGNOSTIC ONLY, 0 in any real use: nonzero bits make the dense
+                              screen skip work so its pipeline stages can be timed apart (results are
+                              then WRONG): 1 = no screening math, 2 = no TMEM loads either,
+                              4 = producers ignore their twins' progress, 8 = no candidate path */
 } sofa_tuning;
 
 int sofa_default_tuning(sofa_tuning* out);
@@ -189,8 +198,9 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
 
 /* Seed bound for sharded search (the optional best-so-far exchange of BASELINE.json's
  * north_star): per query, the k-th smallest squared z-ED among the rows this index's seed step
- * refines (the own-key leaf, MESSI's approximate search P:169, and the 32 lowest word LBs of the
- * lowest-LB leaves), +inf if fewer than k.  The minimum of it over shards bounds the GLOBAL k-th
+ * refines (the lowest-LB words of the query's own-key leaf, MESSI's approximate search P:169 — the
+ * query tables and that one leaf, no tree descent), +inf if fewer than k.  The minimum of it over
+ * shards bounds the GLOBAL k-th
  * best, so passing that minimum as `bsf_init` to every shard's sofa_knn prunes shards that do not
  * hold the neighbours without changing the merged result.
  *   queries_dev: q x len float32; out_bound_dev: q float32.  Device pointers.  Errors: EINVAL, ECUDA. */

@@ -283,7 +283,7 @@ struct sofa_index {
   float2* stats_orig = nullptr;   // n, original row order (dense path)
   __nv_bfloat16* xb16 = nullptr;  // n x xb_ld, original row order: z-normalised rows in bfloat16 (dense screen)
   int xb_ld = 0;                  // row stride of xb16 (len rounded up to 8: 16-byte TMA rows)
-  int32_t dense_permille = 100;   // dense path when >= this many permille of blocks survive (0: off)
+  int32_t dense_permille = 20;    // dense path when >= this many permille of probed words pass (0: off)
   double build_ms[4] = {};        // model, transform, sort, gather + envelopes (CUDA events)
   DenseScratch dense;
   int32_t* perm = nullptr;        // n: sorted position -> local row
@@ -344,7 +344,11 @@ int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_
                  float* ed_out = nullptr, int64_t* lb_rows = nullptr, float* seed_out = nullptr);
 // batch-level dense decision (f1): run the tensor-core pass iff the flagged queries' estimated sparse
 // refines add up to at least one full pass over the shard's rows
-inline int64_t dense_batch_rows(const sofa_index* ix) { return ix->n > 0 ? ix->n : 1; }
+// the batch decision: the dense pass runs iff the flagged queries' estimated sparse refines add up to at
+// least this many rows (default: one pass over the rows)
+inline int64_t dense_batch_rows(const sofa_index* ix) {
+  return ix->tune.dense_batch_rows > 0 ? ix->tune.dense_batch_rows : (ix->n > 0 ? ix->n : 1);
+}
 int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stats, cudaStream_t st);
 int ensure_dense_scratch(sofa_index* ix, int q, int k);
 int dense_dots(const float* rows, int64_t m, int len, const float* queries, int q, float* out, cudaStream_t st);

@@ -45,10 +45,10 @@ namespace sofa {
 constexpr int DM = 128;                  // rows per tile (MMA M = TMEM lanes)
 constexpr int DKC = 64;                  // bf16 per K chunk = 128-byte rows (SWIZZLE_128B atom)
 constexpr int DA_BYTES = DM * DKC * 2;   // 16 KB per A stage
-constexpr int D_THREADS = 320;           // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2..9 epilogue
+constexpr int D_THREADS = 352;           // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2..9 epilogue (2 groups),
+                                         // warp 10 threshold refresher
 constexpr int D_AHEAD = 8;               // row tiles a CTA may run ahead of its twins
 constexpr int D_MAX_STAGES = 8;          // A ring depth cap (barrier arrays)
-constexpr int D_REFRESH = 16;            // tiles between re-reads of the other CTAs' thresholds
 constexpr int D_SMEM_MAX = 232448 - 2048;  // opt-in shared memory per CTA on sm_100, less the static part
 constexpr int D_MISC = 4096;             // per-query thresholds / norms + barriers
 
@@ -132,8 +132,9 @@ struct DenseArgs {
   int* ubn;
   int* ub_lock;
   unsigned long long* cand;  // (slot << 32) | row
-  int64_t cand_cap;
-  unsigned long long* cand_count;
+  int64_t cand_cap;  // split into one slice per CTA (cand_cap / gridDim.x entries each)
+  int* slice_count;  // per CTA: candidates emitted (may exceed the slice: overflow)
+  int streamed;      // STR mode (queries streamed with the rows; n = 1024) vs RES (queries resident)
   int* overflow;  // per slot flag
   int* ovf_list;
   int* ovf_count;
@@ -141,24 +142,8 @@ struct DenseArgs {
   float* raw_out; // debug (sofa_dense_dots): write the raw dot products, rows x raw_ld, no screening
   int raw_ld;
   int raw_q;      // debug: number of query slots (instead of *qd_count)
+  int diag;       // sofa_tuning.dense_diag (timing diagnostics; 0 in real use)
 };
-
-__device__ __forceinline__ void emit_candidate(const DenseArgs& A, bool pass, int slot, uint32_t row) {
-  const unsigned m = __ballot_sync(FULL, pass);
-  if (!m) return;
-  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-  unsigned long long base = 0;
-  if (lane == leader) base = atomicAdd(A.cand_count, (unsigned long long)__popc(m));
-  base = __shfl_sync(FULL, base, leader);
-  if (pass) {
-    const unsigned long long pos = base + __popc(m & ((1u << lane) - 1u));
-    if (pos < (unsigned long long)A.cand_cap) {
-      A.cand[pos] = ((unsigned long long)slot << 32) | row;
-    } else if (atomicExch(&A.overflow[slot], 1) == 0) {
-      A.ovf_list[atomicAdd(A.ovf_count, 1)] = slot;
-    }
-  }
-}
 
 // shared-memory float minimum (values of either sign), rare path
 __device__ __forceinline__ void smem_fmin(float* p, float v) {
@@ -171,12 +156,45 @@ __device__ __forceinline__ void smem_fmin(float* p, float v) {
   }
 }
 
+// Per-CTA k-smallest UB lists (k > 1): col x k floats, counts, locks, in shared memory when they fit.
+struct UbLists {
+  float* l;
+  int* n;
+  int* lock;
+};
+
 // a candidate row's upper bound UB_g lowers the query's threshold: k = 1 directly; k > 1 through
-// the k smallest UBs of distinct candidate rows (each row is screened once per query)
-__device__ void offer_ub(const DenseArgs& A, int slot, float ub, float* s_d, float eps_minus_qn) {
+// the k smallest UBs of distinct candidate rows (each row is screened once per query, by one CTA).
+// s_d is this CTA's copy (thr + eps - |q^|^2); an offer that cannot lower it is skipped (every bound
+// stays valid).  With per-CTA lists (L.l != nullptr) the k-th smallest UB of the rows THIS CTA
+// screened is the CTA's bound (k distinct rows), pushed to the global threshold by atomicMin; no
+// global lock.  Otherwise one global list per query under a spin lock.
+__device__ void offer_ub(const DenseArgs& A, int slot, int col, float ub, float* s_d, float eps_minus_qn,
+                         const UbLists& L) {
+  if (!(ub + eps_minus_qn < *(volatile float*)s_d)) return;
   float t = INFINITY;
   if (A.k == 1) {
     t = ub;
+  } else if (L.l) {
+    int* lk = &L.lock[col];
+    while (atomicCAS(lk, 0, 1) != 0) {
+    }
+    __threadfence_block();
+    volatile float* l = L.l + col * A.k;
+    const int n = *(volatile int*)&L.n[col];
+    if (n < A.k || ub < l[n - 1]) {
+      int p = n < A.k ? n : A.k - 1;
+      while (p > 0 && l[p - 1] > ub) {
+        l[p] = l[p - 1];
+        --p;
+      }
+      l[p] = ub;
+      const int nn = n < A.k ? n + 1 : A.k;
+      *(volatile int*)&L.n[col] = nn;
+      if (nn == A.k) t = l[A.k - 1];
+    }
+    __threadfence_block();
+    atomicExch(lk, 0);
   } else {
     int* lk = &A.ub_lock[slot];
     while (atomicCAS(lk, 0, 1) != 0) {
@@ -204,20 +222,63 @@ __device__ void offer_ub(const DenseArgs& A, int slot, float ub, float* s_d, flo
   }
 }
 
-// Row tiles of CTA b: with g query groups and c = G / g CTAs per group, CTA b serves group b % g and
-// row tiles (b / g) + j c; CTAs b >= c g idle.  "Twins": CTAs with the same b / g (same tiles).
+// The candidates of one 32-column chunk (rare path): m = this lane's passing columns.  One shared-memory
+// atomic per warp reserves their slots in this CTA's slice of the candidate buffer; each passing (row,
+// query) then offers its UB_g.
+__device__ void emit_chunk(const DenseArgs& A, uint32_t m, const uint32_t (&v)[32], int c0, int q0, uint32_t row,
+                           float xn, float* s_d, const float* s_qn, const float* s_eps, int* s_ccount,
+                           unsigned long long* slice, int64_t slice_cap, const UbLists& L) {
+  const int lane = threadIdx.x & 31;
+  const int cnt = __popc(m);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const int total = __shfl_sync(FULL, incl, 31);
+  int base = 0;
+  if (lane == 0 && total) base = atomicAdd(s_ccount, total);
+  base = __shfl_sync(FULL, base, 0) + incl - cnt;
+  while (m) {
+    const int c = __ffs(m) - 1;
+    m &= m - 1;
+    const int col = c0 + c, slot = q0 + col;
+    if (base < slice_cap) {
+      slice[base] = ((unsigned long long)slot << 32) | row;
+    } else if (atomicExch(&A.overflow[slot], 1) == 0) {
+      A.ovf_list[atomicAdd(A.ovf_count, 1)] = slot;
+    }
+    ++base;
+    float dot = 0.f;
+#pragma unroll
+    for (int u = 0; u < 32; ++u)  // select without dynamic register indexing
+      if (u == c) dot = __uint_as_float(v[u]);
+    const float ub = (s_qn[col] + xn - 2.f * dot) + s_eps[col];
+    offer_ub(A, slot, col, ub, s_d + col, s_eps[col] - s_qn[col], L);
+  }
+}
+
+// Work of CTA b: with g query groups and c = G / g CTAs per group, CTA b serves group b % g and work
+// units (b / g) + j c; CTAs b >= c g idle.  "Twins": CTAs with the same b / g (same units).  A unit is
+// one row tile with the group's queries resident in shared memory (RES: rows n <= 512), or two row
+// tiles sharing the query chunks streamed next to them (STR: the queries do not fit, n = 1024).
 __global__ void __launch_bounds__(D_THREADS, 1)
     k_dense_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const DenseArgs A) {
   extern __shared__ __align__(1024) unsigned char dsm_raw[];
-  unsigned char* dsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by pointer arithmetic on the shared array (keeps the shared address space visible to
+  // the compiler: LDS, not generic loads, for the per-query vectors below)
+  unsigned char* dsm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
   __shared__ uint32_t s_tmem;
-  __shared__ uint64_t bars[2 * 8 + 5];
+  __shared__ uint64_t bars[2 * D_MAX_STAGES + 5];
+  __shared__ int s_done, s_ccount;
 
   const int qd = A.raw_out ? A.raw_q : *A.qd_count;
   if (qd == 0) return;
   if (!A.raw_out && *reinterpret_cast<const unsigned long long*>(A.qd_count + 6) < (unsigned long long)A.dense_rows)
     return;  // batch decision: sparse (the deferred k_query launch finishes the flagged queries)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool str = A.streamed != 0;
   const int ng = (qd + A.nq_max - 1) / A.nq_max;               // query groups
   const int nq = ((qd + ng - 1) / ng + 15) / 16 * 16;          // columns per group (MMA N), <= nq_max
   const int G = gridDim.x, b = blockIdx.x;
@@ -226,18 +287,33 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   const int grp = b % ng, twin = b / ng;
   const int q0 = grp * nq, nqv = qd - q0 < nq ? qd - q0 : nq;  // valid columns of this group
   const int KC = A.KC;
-  int S = (A.smem_dyn - 1024 - KC * nq * 128 - D_MISC) / DA_BYTES;  // as deep as the queries leave room for
+  const int bres = str ? 0 : KC * nq * 128;                    // resident query bytes (RES)
+  const int sbytes = str ? 2 * DA_BYTES + nq * 128 : DA_BYTES; // one ring stage: a K chunk of the unit
+  // k > 1: per-CTA UB lists in shared memory if they fit next to a ring of >= 3 stages (else global)
+  const int lbytes = A.k > 1 ? (nq * A.k * 4 + nq * 8 + 15) / 16 * 16 : 0;
+  const bool local_lists = A.k > 1 && !A.raw_out && A.smem_dyn - 1024 - bres - D_MISC - lbytes >= 3 * sbytes;
+  int S = (A.smem_dyn - 1024 - bres - D_MISC - (local_lists ? lbytes : 0)) / sbytes;  // as deep as the rest allows
   S = S > D_MAX_STAGES ? D_MAX_STAGES : S;
-  unsigned char* sB = dsm;                                     // KC x nq x 128 B (resident)
-  unsigned char* sA = dsm + (size_t)KC * nq * 128;             // S x 16 KB
-  float* s_d = reinterpret_cast<float*>(sA + (size_t)S * DA_BYTES);  // nq: thr + eps - |q^|^2
-  float* s_qn = s_d + 256;                                            // nq: |q^|^2
-  float* s_eps = s_qn + 256;                                          // nq: eps
-  uint64_t* full = bars;           // [S]
-  uint64_t* empty = bars + 8;      // [S]
-  uint64_t* tfull = bars + 16;     // [2]
-  uint64_t* tempty = bars + 18;    // [2]
-  uint64_t* bfull = bars + 20;
+  unsigned char* sB = dsm;                                     // RES: KC x nq x 128 B
+  unsigned char* sA = dsm + bres;                              // S stages
+  float* s_d = reinterpret_cast<float*>(sA + (size_t)S * sbytes);  // nq: thr + eps - |q^|^2
+  float* s_qn = s_d + 256;                                         // nq: |q^|^2
+  float* s_eps = s_qn + 256;                                       // nq: eps
+  UbLists L{nullptr, nullptr, nullptr};
+  if (local_lists) {
+    L.l = s_eps + 256;           // nq x k
+    L.n = reinterpret_cast<int*>(L.l + nq * A.k);
+    L.lock = L.n + nq;
+  }
+  uint64_t* full = bars;                   // [S]
+  uint64_t* empty = bars + D_MAX_STAGES;   // [S]
+  uint64_t* tfull = bars + 2 * D_MAX_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bfull = tfull + 4;
+  const int64_t T = A.n_tiles;
+  const int64_t U = str ? (T + 1) / 2 : T;  // work units
+  const int64_t slice_cap = A.cand_cap / G;
+  unsigned long long* slice = A.cand + (int64_t)b * slice_cap;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
@@ -246,9 +322,11 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 8 * 32);
+      mbar_init(&tempty[s], 4 * 32);  // the 4 warps of epilogue group s
     }
     mbar_init(bfull, 1);
+    s_done = 0;
+    s_ccount = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -264,6 +342,10 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     s_d[c] = d;
     s_qn[c] = qn;
     s_eps[c] = e;
+    if (L.l && c < nq) {
+      L.n[c] = 0;
+      L.lock[c] = 0;
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem))
@@ -274,23 +356,23 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
-  const int64_t T = A.n_tiles;
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
-      // the group's queries: every K chunk, 16 rows per box, resident for the whole pass
-      mbar_expect_tx(bfull, (uint32_t)(KC * nq * 128));
-      for (int kc = 0; kc < KC; ++kc)
-        for (int r = 0; r < nq; r += 16) tma_load_2d(sB + ((size_t)kc * nq + r) * 128, &tmB, kc * DKC, q0 + r, bfull);
+      if (!str) {  // the group's queries: every K chunk, 16 rows per box, resident for the whole pass
+        mbar_expect_tx(bfull, (uint32_t)(KC * nq * 128));
+        for (int kc = 0; kc < KC; ++kc)
+          for (int r = 0; r < nq; r += 16) tma_load_2d(sB + ((size_t)kc * nq + r) * 128, &tmB, kc * DKC, q0 + r, bfull);
+      }
       volatile int* prog = A.progress;
       int stage = 0;
       uint32_t phase = 0;
       int64_t j = 0;
       int twin_lo = 0;  // the slowest twin's progress, re-read only when this CTA would run too far ahead
-      for (int64_t t = twin; t < T; t += cpg, ++j) {
-        if (ng > 1 && twin_lo < j - D_AHEAD) {  // stay within D_AHEAD tiles of the twins (the tile is still
-          for (;;) {                            // in L2 when they read it)
+      for (int64_t u = twin; u < U; u += cpg, ++j) {
+        if (ng > 1 && !(A.diag & 4) && twin_lo < j - D_AHEAD) {  // stay within D_AHEAD units of the twins
+          for (;;) {                                              // (the tile is still in L2 when they read it)
             int lo = 0x7fffffff;
             for (int o = 0; o < ng; ++o) {
               const int p = prog[twin * ng + o];
@@ -303,8 +385,15 @@ __global__ void __launch_bounds__(D_THREADS, 1)
         }
         for (int kc = 0; kc < KC; ++kc) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], DA_BYTES);
-          tma_load_2d(sA + stage * DA_BYTES, &tmA, kc * DKC, (int)(t * DM), &full[stage]);
+          unsigned char* st = sA + (size_t)stage * sbytes;
+          mbar_expect_tx(&full[stage], (uint32_t)sbytes);
+          if (!str) {
+            tma_load_2d(st, &tmA, kc * DKC, (int)(u * DM), &full[stage]);
+          } else {
+            tma_load_2d(st, &tmA, kc * DKC, (int)(2 * u * DM), &full[stage]);
+            tma_load_2d(st + DA_BYTES, &tmA, kc * DKC, (int)((2 * u + 1) * DM), &full[stage]);
+            for (int r = 0; r < nq; r += 16) tma_load_2d(st + 2 * DA_BYTES + r * 128, &tmB, kc * DKC, q0 + r, &full[stage]);
+          }
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -318,62 +407,108 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     // ---------------------------------------------------------------- MMA issuer (one thread)
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(nq);
-      mbar_wait(bfull, 0);
+      if (!str) mbar_wait(bfull, 0);
       tc_fence_after();
       int stage = 0;
       uint32_t phase = 0;
       int64_t j = 0;
-      for (int64_t t = twin; t < T; t += cpg, ++j) {
-        const int acc = (int)(j & 1);
-        const uint32_t aph = (uint32_t)((j >> 1) & 1);
-        mbar_wait(&tempty[acc], aph ^ 1);
+      for (int64_t u = twin; u < U; u += cpg, ++j) {
+        const int acc = str ? 0 : (int)(j & 1);
+        if (!str) {
+          mbar_wait(&tempty[acc], (uint32_t)((j >> 1) & 1) ^ 1);
+        } else {  // both buffers: the unit's two tiles
+          mbar_wait(&tempty[0], (uint32_t)(j & 1) ^ 1);
+          mbar_wait(&tempty[1], (uint32_t)(j & 1) ^ 1);
+        }
         tc_fence_after();
-        const uint32_t dt = tmem + (uint32_t)(acc * 256);
         for (int kc = 0; kc < KC; ++kc) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * DA_BYTES);
-          const uint32_t b0 = smem_u32(sB + (size_t)kc * nq * 128);
+          const uint32_t a0 = smem_u32(sA + (size_t)stage * sbytes);
+          if (!str) {
+            const uint32_t b0 = smem_u32(sB + (size_t)kc * nq * 128);
+            const uint32_t dt = tmem + (uint32_t)(acc * 256);
 #pragma unroll
-          for (int kk = 0; kk < DKC / 16; ++kk)  // UMMA_K = 16 bf16 = 32 bytes along the swizzled row
-            tc_mma_bf16(dt, sdesc_sw128(a0 + 32 * kk), sdesc_sw128(b0 + 32 * kk), idesc, (kc | kk) ? 1u : 0u);
+            for (int kk = 0; kk < DKC / 16; ++kk)  // UMMA_K = 16 bf16 = 32 bytes along the swizzled row
+              tc_mma_bf16(dt, sdesc_sw128(a0 + 32 * kk), sdesc_sw128(b0 + 32 * kk), idesc, (kc | kk) ? 1u : 0u);
+          } else {
+            const uint32_t b0 = a0 + 2 * DA_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < DKC / 16; ++kk) {
+              tc_mma_bf16(tmem, sdesc_sw128(a0 + 32 * kk), sdesc_sw128(b0 + 32 * kk), idesc, (kc | kk) ? 1u : 0u);
+              tc_mma_bf16(tmem + 256, sdesc_sw128(a0 + DA_BYTES + 32 * kk), sdesc_sw128(b0 + 32 * kk), idesc,
+                          (kc | kk) ? 1u : 0u);
+            }
+          }
           tc_commit(&empty[stage]);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);
+        if (!str) {
+          tc_commit(&tfull[acc]);
+        } else {
+          tc_commit(&tfull[0]);
+          tc_commit(&tfull[1]);
+        }
       }
+      *(volatile int*)&s_done = 1;  // every MMA issued: the threshold refresher may stop
     }
+  } else if (warp == D_THREADS / 32 - 1) {
+    // ---------------------------------------------------------------- threshold refresher
+    // other CTAs' improvements of the group's thresholds (global) into this CTA's copy, off the
+    // epilogue's path
+    if (!A.raw_out)
+      while (!*(volatile int*)&s_done) {
+        for (int c = lane; c < nqv; c += 32) {
+          const float nd = *(volatile float*)&A.thr[q0 + c] + s_eps[c] - s_qn[c];
+          if (nd < s_d[c]) smem_fmin(s_d + c, nd);
+        }
+        __nanosleep(1000);
+      }
   } else {
-    // ---------------------------------------------------------------- epilogue (8 warps)
-    // warp w reads TMEM lane quarter w % 4 (its 32 rows of the tile) and every other 16-column chunk
-    // (half (w - 2) / 4).  Per element: val = 2 dot + (thr + eps - |q^|^2); the row is a candidate
-    // for that query iff val >= |x^|^2 (LB_g <= thr).
-    const int qtr = warp & 3, half = (warp - 2) >> 2;
+    // ---------------------------------------------------------------- epilogue (2 groups x 4 warps)
+    // Group g = (warp - 2) / 4 owns accumulator buffer g.  RES: this CTA's tiles j = g, g + 2, ...: while
+    // one group screens its tile the MMA fills the other buffer and the other group screens the previous
+    // tile, so a group has two MMA tile-times per tile.  STR: the two tiles of each unit.  Warp w reads
+    // TMEM lane quarter w % 4 (its 32 rows of the tile) and every 32-column chunk.  Per element:
+    // val = 2 dot + (thr + eps - |q^|^2); the row is a candidate for that query iff val >= |x^|^2
+    // (LB_g <= thr).
+    const int qtr = warp & 3, grp_e = (warp - 2) >> 2;
     const int r = qtr * 32 + lane;
     const int nch = (nq + 31) / 32;  // 32-column chunks (columns past the group's queries have s_d = -inf)
     const float nlen = (float)A.len;
-    int64_t j = 0;
-    auto xnorm = [&](int64_t tt) {  // |x^|^2 of this thread's row of tile tt: n, 0 for a constant row, NaN past N
-      const int64_t rr = tt * DM + r;
-      if (rr >= A.n || tt >= T) return __int_as_float(0x7fffffff);
-      if (A.raw_out) return 0.f;
-      return A.stats_orig[rr].y > 0.f ? nlen : 0.f;
+    // the i-th tile of this group
+    auto exists = [&](int64_t i) -> bool { return str ? twin + i * cpg < U : twin + (2 * i + grp_e) * cpg < U; };
+    auto tile_of = [&](int64_t i) -> int64_t { return str ? 2 * (twin + i * cpg) + grp_e : twin + (2 * i + grp_e) * cpg; };
+    // the row's 1/sigma, loaded a tile (of this group) ahead; |x^|^2 = n, 0 for a constant row, NaN past N
+    auto sig_load = [&](int64_t i) -> float {
+      const int64_t tt = tile_of(i), rr = tt * DM + r;
+      if (!exists(i) || rr >= A.n || tt >= T) return __int_as_float(0x7fffffff);
+      if (A.raw_out) return 1.f;
+      return A.stats_orig[rr].y;
     };
-    float xn_next = xnorm(twin);
-    for (int64_t t = twin; t < T; t += cpg, ++j) {
-      const int acc = (int)(j & 1);
-      const uint32_t aph = (uint32_t)((j >> 1) & 1);
-      const int64_t row = t * DM + r;
-      const float xn = xn_next;  // loaded one tile ahead
-      xn_next = xnorm(t + cpg);
+    auto xnorm_of = [&](float sig) -> float { return isnan(sig) ? sig : (sig > 0.f ? nlen : 0.f); };
+    const int acc = grp_e;
+    float sig_next = sig_load(0);
+    for (int64_t i = 0; exists(i); ++i) {
+      const uint32_t aph = (uint32_t)(i & 1);
+      const int64_t row = tile_of(i) * DM + r;
+      const float sig = sig_next;  // loaded one group tile ahead
+      sig_next = sig_load(i + 1);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
+      const float xn = xnorm_of(sig);
+      if (A.diag & 2) {  // timing diagnostic: release the buffer unread
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        continue;
+      }
       const uint32_t tbase = tmem + ((uint32_t)(qtr * 32) << 16) + (uint32_t)(acc * 256);
       // screen 32 columns held in v (registers): val = 2 dot + (thr + eps - |q^|^2) >= |x^|^2 ?
       auto screen = [&](const uint32_t (&v)[32], int c0) {
+        if (A.diag & 1) return;  // timing diagnostic: TMEM loads only
         if (A.raw_out) {
           if (row < A.n)
             for (int c = 0; c < 32; ++c)
@@ -390,48 +525,32 @@ __global__ void __launch_bounds__(D_THREADS, 1)
           const float a3 = fmaf(2.f, __uint_as_float(v[c + 3]), d4.w);
           vmax = fmaxf(vmax, fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)));
         }
-        if (__any_sync(FULL, vmax >= xn)) {  // rare: this chunk has candidates
-#pragma unroll 1
-          for (int c = 0; c < 32; ++c) {
-            float dot = 0.f;
+        if (!(A.diag & 8) && __any_sync(FULL, vmax >= xn)) {  // rare: this chunk has candidates
+          uint32_t m = 0;
 #pragma unroll
-            for (int u = 0; u < 32; ++u)  // select without dynamic register indexing
-              if (u == c) dot = __uint_as_float(v[u]);
-            const int col = c0 + c;
-            const bool pass = fmaf(2.f, dot, s_d[col]) >= xn;
-            if (!__any_sync(FULL, pass)) continue;
-            emit_candidate(A, pass, q0 + col, (uint32_t)row);
-            if (pass) {
-              const float ub = (s_qn[col] + xn - 2.f * dot) + s_eps[col];
-              offer_ub(A, q0 + col, ub, s_d + col, s_eps[col] - s_qn[col]);
-            }
-          }
+          for (int c = 0; c < 32; ++c) m |= (fmaf(2.f, __uint_as_float(v[c]), s_d[c0 + c]) >= xn ? 1u : 0u) << c;
+          emit_chunk(A, m, v, c0, q0, (uint32_t)row, xn, s_d, s_qn, s_eps, &s_ccount, slice, slice_cap, L);
         }
       };
       // TMEM loads double-buffered: the next chunk is in flight while this one is screened
       uint32_t va[32], vb[32];
-      if (half < nch) TMEM_LD32(tbase + half * 32, va);
+      TMEM_LD32(tbase, va);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      for (int ch = half; ch < nch; ch += 4) {
-        if (ch + 2 < nch) TMEM_LD32(tbase + (ch + 2) * 32, vb);
+      for (int ch = 0; ch < nch; ch += 2) {
+        if (ch + 1 < nch) TMEM_LD32(tbase + (ch + 1) * 32, vb);
         screen(va, ch * 32);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (ch + 2 >= nch) break;
-        if (ch + 4 < nch) TMEM_LD32(tbase + (ch + 4) * 32, va);
-        screen(vb, (ch + 2) * 32);
+        if (ch + 1 >= nch) break;
+        if (ch + 2 < nch) TMEM_LD32(tbase + (ch + 2) * 32, va);
+        screen(vb, (ch + 1) * 32);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      // other CTAs' improvements of the thresholds (global) into this CTA's copy, now and then
-      if (qtr == 0 && !A.raw_out && (j % D_REFRESH) == D_REFRESH - 1)
-        for (int c = lane + 32 * half; c < nqv; c += 64) {
-          const float nd = *(volatile float*)&A.thr[q0 + c] + s_eps[c] - s_qn[c];
-          if (nd < s_d[c]) smem_fmin(s_d + c, nd);
-        }
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0 && A.slice_count) A.slice_count[b] = s_ccount;  // candidates of this CTA (may exceed its slice)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
@@ -458,7 +577,8 @@ struct DensePost {
   int* lock;
   const unsigned long long* cand;
   int64_t cand_cap;
-  const unsigned long long* cand_count;
+  const int* slice_count;  // per screen CTA
+  int nslices;             // screen CTAs (slices of cand_cap / nslices entries)
   const int* overflow;
   const int* ovf_list;
   const int* ovf_count;
@@ -509,8 +629,23 @@ __global__ void __launch_bounds__(kThreads) k_dense_post(const DensePost P) {
   const int64_t gw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
   const int nf4 = P.len >> 2;
-  const int64_t nc_raw = (int64_t)*P.cand_count;
-  const int64_t nc = nc_raw < P.cand_cap ? nc_raw : P.cand_cap;
+  // the screen CTAs' slices, back to back: prefix of the stored counts
+  __shared__ long long s_pre[1025];
+  const int64_t slice_cap = P.cand_cap / P.nslices;
+  if (threadIdx.x == 0) {
+    long long acc = 0, raw = 0;
+    for (int i = 0; i < P.nslices; ++i) {
+      s_pre[i] = acc;
+      const long long c = P.slice_count[i];
+      raw += c;
+      acc += c < slice_cap ? c : slice_cap;
+    }
+    s_pre[P.nslices] = acc;
+    s_pre[1024] = raw;
+  }
+  __syncthreads();
+  const int64_t nc_raw = s_pre[1024];
+  const int64_t nc = s_pre[P.nslices];
   const int nov = *P.ovf_count;
   const int64_t total = nc + (int64_t)nov * P.n;
   unsigned int n_ref = 0;
@@ -518,7 +653,12 @@ __global__ void __launch_bounds__(kThreads) k_dense_post(const DensePost P) {
     int slot;
     int64_t row;
     if (u < nc) {
-      const unsigned long long e = P.cand[u];
+      int lo = 0, hi = P.nslices;  // the slice holding entry u: s_pre[lo] <= u < s_pre[lo + 1]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_pre[mid] <= u) lo = mid; else hi = mid;
+      }
+      const unsigned long long e = P.cand[lo * slice_cap + (u - s_pre[lo])];
       slot = (int)(e >> 32);
       row = (int64_t)(uint32_t)e;
       if (P.overflow[slot]) continue;  // the fallback below rescans that slot completely
@@ -603,11 +743,17 @@ static int make_tmap_bf16(CUtensorMap* m, const __nv_bfloat16* base, int64_t row
 // launch geometry of the screen for row length `len`: the queries per group that fit next to an A ring
 // of at least 4 stages (multiple of 16, <= 256 for the 2 x 256 TMEM accumulator columns); the kernel
 // then deepens the ring into whatever its group's queries leave free (up to D_MAX_STAGES)
-static void dense_geometry(int len, int& nq_max) {
+static void dense_geometry(int len, int& nq_max, int& streamed) {
   const int KC = (len + DKC - 1) / DKC;
   const int avail = D_SMEM_MAX - 1024 - 4 * DA_BYTES - D_MISC;
   const int nq = avail / (KC * 128) / 16 * 16;
-  nq_max = nq > 256 ? 256 : nq;
+  if (nq >= 128) {  // RES: queries resident next to a ring of >= 4 row-tile stages
+    nq_max = nq > 256 ? 256 : nq;
+    streamed = 0;
+  } else {          // STR: 256 queries per group, streamed with 2 row tiles per stage (3 x 64 KB stages)
+    nq_max = 256;
+    streamed = 1;
+  }
 }
 
 static int launch_screen(sofa_index* ix, const CUtensorMap& tmA, const CUtensorMap& tmB, const DenseArgs& A,
@@ -642,7 +788,7 @@ static void fill_screen_args(sofa_index* ix, int k, DenseArgs& A) {
   A.k = k;
   A.KC = (ix->len + DKC - 1) / DKC;
   A.n_tiles = (ix->n + DM - 1) / DM;
-  dense_geometry(ix->len, A.nq_max);
+  dense_geometry(ix->len, A.nq_max, A.streamed);
   A.smem_dyn = D_SMEM_MAX;
   A.stats_orig = ix->stats_orig;
   A.qd_count = D.counters;
@@ -653,11 +799,12 @@ static void fill_screen_args(sofa_index* ix, int k, DenseArgs& A) {
   A.ub_lock = D.ub_lock;
   A.cand = D.cand;
   A.cand_cap = D.cand_cap;
-  A.cand_count = reinterpret_cast<unsigned long long*>(D.counters + 2);
+  A.slice_count = D.counters + 64 + 1024;
   A.overflow = D.overflow;
   A.ovf_list = D.ovf_list;
   A.ovf_count = D.counters + 1;
   A.progress = D.counters + 64;
+  A.diag = ix->tune.dense_diag;
 }
 
 int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stats, cudaStream_t st) {
@@ -696,7 +843,8 @@ int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stat
   P.lock = D.lock;
   P.cand = D.cand;
   P.cand_cap = D.cand_cap;
-  P.cand_count = A.cand_count;
+  P.slice_count = A.slice_count;
+  P.nslices = ix->sms;
   P.overflow = D.overflow;
   P.ovf_list = D.ovf_list;
   P.ovf_count = D.counters + 1;
@@ -754,7 +902,7 @@ int dense_dots(const float* rows, int64_t m, int len, const float* queries, int 
     A.k = 1;
     A.KC = (len + DKC - 1) / DKC;
     A.n_tiles = (m + DM - 1) / DM;
-    dense_geometry(len, A.nq_max);
+    dense_geometry(len, A.nq_max, A.streamed);
     A.smem_dyn = D_SMEM_MAX;
     A.progress = prog;
     A.raw_out = out;
@@ -770,7 +918,7 @@ int dense_dots(const float* rows, int64_t m, int len, const float* queries, int 
 }
 
 // scratch for q queries at k (grown on demand); counters: [0] dense slots, [1] overflow slots,
-// [2..3] candidate count (u64), [4] done CTAs, [6..7] estimated refines; [64..] per-CTA progress.
+// [4] done CTAs, [6..7] estimated refines; [64..] per-CTA progress; [64 + 1024..] per-CTA candidates.
 int ensure_dense_scratch(sofa_index* ix, int q, int k) {
   DenseScratch& D = ix->dense;
   if (D.q_cap >= q && D.k_cap >= k && D.len == ix->len) return SOFA_OK;
@@ -797,7 +945,7 @@ int ensure_dense_scratch(sofa_index* ix, int q, int k) {
   SOFA_CK(cudaMalloc(&D.overflow, (size_t)q * 4));
   SOFA_CK(cudaMalloc(&D.ovf_list, (size_t)q * 4));
   SOFA_CK(cudaMalloc(&D.cand, (size_t)D.cand_cap * 8));
-  SOFA_CK(cudaMalloc(&D.counters, 64 * 4 + 1024 * 4));  // counters, then per-CTA progress
+  SOFA_CK(cudaMalloc(&D.counters, 64 * 4 + 2048 * 4));  // counters, per-CTA progress, per-CTA candidate counts
   return SOFA_OK;
 }
 

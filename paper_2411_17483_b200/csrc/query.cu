@@ -63,7 +63,9 @@ struct ScanTask {
   int q;
   int cnt_flags;  // leaves | sorted << 30
 };
-constexpr int kTaskSorted = 1 << 30, kTaskCnt = (1 << 29) - 1;
+// cnt_flags: leaf count | sorted list | range task (off = first leaf, no pool entries: every leaf of
+// [off, off + cnt) in storage order)
+constexpr int kTaskSorted = 1 << 30, kTaskRange = 1 << 29, kTaskCnt = (1 << 29) - 1;
 
 struct QArgs {
   const float* series;
@@ -88,9 +90,9 @@ struct QArgs {
   int* qcounter;
   unsigned long long* dstats;
   long long* trace;  // nullable: per query SOFA_TRACE_FIELDS int64
-  // dense path (f1, dense.cu): a query whose leaf list keeps >= dense_min blocks after its
-  // TAKE0 (8) lowest-LB blocks were refined is handed over (0 = never)
-  int64_t dense_min;
+  // dense path (f1, dense.cu): a query for which >= dense_pm permille of a strided word probe pass
+  // its seed threshold is handed over before the tree descent (0 = never)
+  int dense_pm;
   int64_t dense_rows;  // batch decision: dense pass iff the flagged queries' estimated refines >= this
   int dense_force;     // dense_permille >= 1000: every query with a surviving leaf goes dense (tests)
   int mode;            // 0: front, 1: scan, 2: lower-bound evaluation (sofa_lower_bounds), 3: seed bound
@@ -102,7 +104,7 @@ struct QArgs {
   int rev_rounds;     // scan_blocks: refine rounds per unit before it is deferred to the revisit pass
   int topm_min, topm_leaves;  // top-M seeding for lists longer than topm_min, over ~topm_leaves leaves
   QState* qs;          // q
-  float* q_T;          // q x LT x 256 word-LB tables
+  float* q_T;          // q x 3 x LT x 256: word-LB table T, then (range tasks only) Tlo, Thi
   float* q_hat;        // q x len z-normalised queries
   unsigned long long* pool;  // q x nb leaf entries (LB, block)
   unsigned long long* pool_used;
@@ -282,7 +284,10 @@ __host__ __device__ constexpr int refine_rows() { return NF <= 4 ? 2 : 1; }
 // warp's improvement prunes the other warps' candidates at once; no CTA barrier inside the loop.
 template <int LT, int NF, int RR = refine_rows<NF>()>
 __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long* list, int cnt, bool sorted,
-                            const float* s_T, float* s_tkd, int* s_tki, const float4* s_qh4, int seed_rounds = 0) {
+                            const float* s_T, float* s_tkd, int* s_tki, const float4* s_qh4, int seed_rounds = 0,
+                            int64_t range0 = 0, const float* s_env = nullptr) {
+  // list == nullptr: the leaves range0, range0 + 1, ... in storage order, each pruned by its envelope LB
+  // (Tlo = s_env, Thi = s_env + LT * 256) before its words are read
   constexpr int NC = LT / 16;
   constexpr int WMAX = 8 / NC;                          // words per lane per unit
   constexpr int R = RR;  // rows refined together per warp
@@ -324,7 +329,19 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
       const int u = pass == 0 ? idx : s_rev_u[idx];
       const unsigned long long done_key = pass == 0 ? 0ull : s_rev_k[idx];  // refined in pass 0: keys <= this
       const int e = u / ppl, part = u % ppl;
-      const unsigned long long ent = list[e];
+      unsigned long long ent;
+      if (list) {
+        ent = list[e];
+      } else {  // range task: the leaf's envelope LB, lane j < LT takes position j
+        const int64_t leaf = range0 + e;
+        const uint8_t* ev = A.env + leaf * 2 * A.WS;
+        float lbe = 0.f;
+        if (lane < LT && lane < A.l) lbe = s_env[lane * 256 + ev[lane]] + s_env[(LT + lane) * 256 + ev[A.WS + lane]];
+        if (LT > 32 && lane + 32 < A.l)
+          lbe += s_env[(lane + 32) * 256 + ev[lane + 32]] + s_env[(LT + lane + 32) * 256 + ev[A.WS + lane + 32]];
+        lbe = warp_sum_f32(lbe);
+        ent = pack(lbe, (uint32_t)leaf);
+      }
       if (lb_of(ent) > thr) {
         if (sorted && pass == 0) break;  // every later leaf has a larger LB
         continue;
@@ -508,10 +525,45 @@ __device__ void publish_tasks(const QArgs& A, QShared& S, int q, const unsigned 
   __syncthreads();
 }
 
+// front: every leaf of the index as range tasks of the dense-candidate set (a query sent to the dense
+// path before its tree descent; scanned only if the batch skips the dense pass)
+template <int LT>
+__device__ void publish_range(const QArgs& A, QShared& S, int q) {
+  const int64_t n = A.nb;
+  if (n <= 0) return;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int64_t CH = chunk_blocks<LT>(A.B);
+    const int left = A.rank_cap - S.ntask;
+    if (left <= 0) __trap();
+    if ((n + CH - 1) / CH > left) CH = (n + left - 1) / left;
+    S.chsz = (int)CH;
+    S.chunk = S.ntask;
+    S.ntask += (int)((n + CH - 1) / CH);
+    atomicMax(&A.counters[2], S.ntask);
+  }
+  __syncthreads();
+  const int CH = S.chsz;
+  const int nt = (int)((n + CH - 1) / CH);
+  const int r0 = S.chunk;
+  ScanTask* tasks = A.tasks + (int64_t)A.rank_cap * A.q;
+  int* rc = A.rank_count + A.rank_cap;
+  for (int i = tid; i < nt; i += kQThreads) {
+    ScanTask t;
+    t.off = (int64_t)i * CH;
+    t.q = q;
+    t.cnt_flags = (int)(n - (int64_t)i * CH < CH ? n - (int64_t)i * CH : CH) | kTaskRange;
+    const int r = r0 + i;
+    tasks[(int64_t)r * A.q + atomicAdd(&rc[r], 1)] = t;
+  }
+  __syncthreads();
+}
+
 // scan mode: all CTAs pull tasks until the pool is drained; rank-major order (every query's lowest-
 // LB chunk first), so a query's later chunks usually meet its final BSF and are rejected unread
 template <int LT, int NF, int RR = refine_rows<NF>()>
-__device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd, int* s_tki, float4* s_qh4) {
+__device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd, int* s_tki, float4* s_qh4,
+                           float* s_env) {
   const int tid = threadIdx.x;
   bool dense_go = false;
   if (A.qd_counter) {
@@ -526,7 +578,7 @@ __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd,
     for (int i = 0; i < 10; ++i) S.st[i] = 0;
     S.gslot = -1;
   }
-  int cur = -1;
+  int cur = -1, cur_env = -1;
   for (;;) {
     if (tid == 0) {
       int have = 0;
@@ -560,7 +612,7 @@ __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd,
     volatile QState* h = &A.qs[q];
     if (!S.take) {
       if (q != cur) {
-        const float4* T4 = reinterpret_cast<const float4*>(A.q_T + (int64_t)q * LT * 256);
+        const float4* T4 = reinterpret_cast<const float4*>(A.q_T + (int64_t)q * 3 * LT * 256);
         for (int i = tid; i < LT * 64; i += kQThreads) reinterpret_cast<float4*>(s_T)[i] = T4[i];
         for (int i = tid; i < A.len; i += kQThreads) reinterpret_cast<float*>(s_qh4)[i] = A.q_hat[(int64_t)q * A.len + i];
         cur = q;
@@ -574,8 +626,16 @@ __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd,
         S.lock = 0;
       }
       __syncthreads();
-      scan_blocks<LT, NF, RR>(A, S, A.pool + tk.off, tk.cnt_flags & kTaskCnt, (tk.cnt_flags & kTaskSorted) != 0, s_T,
-                          s_tkd, s_tki, s_qh4);
+      const bool range = (tk.cnt_flags & kTaskRange) != 0;
+      if (range && q != cur_env) {  // the query's envelope tables Tlo / Thi (stored by the front)
+        const float4* E4 = reinterpret_cast<const float4*>(A.q_T + ((int64_t)q * 3 + 1) * LT * 256);
+        for (int i = tid; i < 2 * LT * 64; i += kQThreads) reinterpret_cast<float4*>(s_env)[i] = E4[i];
+        cur_env = q;
+        __syncthreads();
+      }
+      scan_blocks<LT, NF, RR>(A, S, range ? nullptr : A.pool + tk.off, tk.cnt_flags & kTaskCnt,
+                              (tk.cnt_flags & kTaskSorted) != 0, s_T, s_tkd, s_tki, s_qh4, 0, range ? tk.off : 0,
+                              s_env);
       __syncthreads();
     }
     if (tid == 0) {
@@ -795,6 +855,54 @@ __device__ void seed_topm(const QArgs& A, QShared& S, const unsigned long long* 
   __syncthreads();
 }
 
+// f1 decision probe: the word LBs (against the query's current threshold) of kProbe words at strided
+// positions of the sorted words; the passing fraction estimates the fraction of ALL rows the sparse path
+// would refine (the stride covers the key order uniformly).  Returns the passing count (every thread).
+constexpr int kProbe = 2048;
+constexpr int kEarlyPermille = 100;     // stage 1 (before the tree descent): >= 10% of the probe passes
+constexpr long long kDenseMinRows = 4096;  // ... and the estimate is at least this many rows
+template <int LT>
+__device__ long long dense_probe(const QArgs& A, QShared& S, const float* s_T) {
+  constexpr int U = 128 / LT;  // words per thread in flight (8 x 16 B at l <= 16)
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t P = A.n < kProbe ? A.n : kProbe;
+  if (tid == 0) S.take = 0;
+  __syncthreads();
+  const float thr = S.thr;
+  int pass = 0;
+  for (int64_t j0 = tid; j0 < P; j0 += (int64_t)kQThreads * U) {
+    uint4 wr[U][LT / 16];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + (int64_t)u * kQThreads;
+      const int64_t pos = j < P ? j * A.n / P : 0;
+#pragma unroll
+      for (int c = 0; c < LT / 16; ++c) wr[u][c] = ld_stream_u4(A.words + pos * A.WS + 16 * c);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (j0 + (int64_t)u * kQThreads < P) pass += word_lb<LT>(wr[u], s_T, thr) <= thr;
+  }
+  pass = __reduce_add_sync(FULL, pass);
+  if (lane == 0 && pass) atomicAdd(&S.take, pass);
+  __syncthreads();
+  const long long npass = S.take;
+  __syncthreads();
+  return npass;
+}
+// flagged: at least `permille` of the probe passes AND that estimate is at least kDenseMinRows rows (a
+// few hundred refines are cheaper than a share of a pass over all rows)
+__device__ __forceinline__ bool dense_flag(const QArgs& A, long long npass, int64_t P, int permille) {
+  return npass * 1000 >= (long long)permille * P && npass * A.n >= kDenseMinRows * P;
+}
+// thread 0: take a dense slot and add the query's estimated sparse refines to the batch decision
+__device__ __forceinline__ int flag_dense(const QArgs& A, long long npass, int64_t P) {
+  const unsigned long long est =
+      A.dense_force ? (unsigned long long)A.dense_rows : (unsigned long long)(npass * A.n / (P > 0 ? P : 1));
+  atomicAdd(reinterpret_cast<unsigned long long*>(A.qd_counter + 6), est);
+  return atomicAdd(A.qd_counter, 1);
+}
+
 template <int LT, int NF, int RR = refine_rows<NF>()>
 __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(const __grid_constant__ QArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -815,7 +923,7 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
   __shared__ uint8_t s_qw[SOFA_MAX_L];
   __shared__ unsigned long long s_seed;
   __shared__ int s_dense;
-  __shared__ long long s_dec[4];  // dense decision inputs: flagged, leaves after take, pass, words
+  __shared__ long long s_dec[4];  // dense decision: flagged (1 stage 1, 2 stage 2), stage-2 pass, stage-1 pass, probe words
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int len = A.len, nf4 = len >> 2, l = A.l, a = A.a;
@@ -823,7 +931,7 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
   unsigned long long* gl2 = gl + A.nb;
 
   if (A.mode == 1) {
-    scan_tasks<LT, NF, RR>(A, S, s_T, s_tkd, s_tki, s_qh4);
+    scan_tasks<LT, NF, RR>(A, S, s_T, s_tkd, s_tki, s_qh4, s_Tlo);
     return;
   }
   for (;;) {
@@ -982,10 +1090,41 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
     scan_blocks<LT, NF, RR>(A, S, &s_seed, A.nb > 0 ? 1 : 0, true, s_T, s_tkd, s_tki, s_qh4,
                             1 + (A.k - 1) / (kQThreads / 32 * RR));
     t_phase[2] = clock64();
+    if (A.mode == 3) {  // sofa_knn_seed: this shard's own-key bound on the k-th best, nothing else
+      if (tid == 0) A.seed_out[qi] = S.tkn == A.k ? S.bsf : INFINITY;
+      __syncthreads();
+      continue;
+    }
+    // ---------------------------------------------------------------- f1: dense-path decision, stage 1
+    // Before the tree descent: a query for which >= 10% of a strided word probe (dense_probe) passes the
+    // seed's threshold is one the SFA bound cannot prune (high-frequency data, noisy members with
+    // sigma = 1): it goes to the batched tensor-core screen (dense.cu) without walking the envelope
+    // tree.  Queries below that are decided again after top-M seeding (stage 2) at dense_pm.
+    if (tid == 0) {
+      s_dense = -1;
+      s_dec[0] = s_dec[1] = s_dec[2] = s_dec[3] = 0;
+    }
+    __syncthreads();
+    if (A.mode == 0 && A.dense_pm > 0) {
+      const long long npass = dense_probe<LT>(A, S, s_T);
+      const int64_t P = A.n < kProbe ? A.n : kProbe;
+      if (tid == 0) {
+        if (A.dense_force || dense_flag(A, npass, P, kEarlyPermille)) {
+          s_dense = flag_dense(A, npass, P);
+          s_dec[0] = 1;
+        }
+        s_dec[2] = npass;
+        s_dec[3] = P;
+      }
+      __syncthreads();
+    }
+    const bool early_dense = s_dense >= 0;
+    if (tid == 0) S.cnt = 0;
+    __syncthreads();
     // ---------------------------------------------------------------- a6: envelope tree descent
     // top level: every node; lower levels: the kFan children of each surviving parent
     // (the MESSI-style tree over sorted SFA-word blocks, P:159-166 / P:171-173)
-    {
+    if (!early_dense) {
       const float thr = S.thr;
       unsigned long long* cur = gl;
       unsigned long long* nxt = gl2;
@@ -1019,11 +1158,6 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
     {
       int cnt = S.cnt;
       if (tid == 0) S.st[6] += cnt;
-      if (A.mode == 3 && cnt > 0 && cnt <= A.topm_min) {  // seed bound of a short list: top-M over all of it
-        for (int i = tid; i < cnt; i += kQThreads) s_blist[i] = gl[i];
-        __syncthreads();
-        seed_topm<LT, NF>(A, S, s_blist, cnt, s_T, s_tkd, s_tki, s_qh4);
-      }
       if (cnt > A.topm_min) {
         // top-M seeding over the TOPM_LEAVES lowest-LB leaves (threshold from a sorted strided sample)
         s_samp[tid] = gl[((int64_t)tid * cnt) / kQThreads];
@@ -1051,66 +1185,17 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
         gl2 = t;
       }
       t_sub[0] = clock64();  // top-M seeding done
-      if (A.mode == 3) {  // sofa_knn_seed: this shard's bound on the k-th best, nothing else
-        if (tid == 0) A.seed_out[qi] = S.tkn == A.k ? S.bsf : INFINITY;
-        __syncthreads();
-        continue;
-      }
-      if (tid == 0) {
-        s_dense = -1;
-        s_dec[0] = s_dec[1] = s_dec[2] = s_dec[3] = 0;
-      }
-      __syncthreads();  // every thread must see -1 before the (uniform) branch below
-      if (A.dense_min > 0 && cnt >= A.dense_min) {
-        // f1 decision, after top-M seeding: sample the words of the TAKE0 lowest-LB leaves (they stay in
-        // the list); if most of them still pass the (nearly final) BSF and many leaves survive, the
-        // SFA bound cannot prune this query and it goes to the batched dense path.
-        constexpr int TAKE0 = 8;
-        s_samp[tid] = gl[((int64_t)tid * cnt) / kQThreads];
-        if (tid == 0) S.take = 0;
-        __syncthreads();
-        bitonic_sort_u64(s_samp, kQThreads);
-        int r = (int)(((int64_t)kQThreads * TAKE0) / cnt);
-        r = r < 0 ? 0 : (r > kQThreads - 1 ? kQThreads - 1 : r);
-        const float tau = lb_of(s_samp[r]);
-        filter_list(gl, cnt, S.thr, tau, s_blist, &S.take, nullptr, nullptr, TAKE0);
-        __syncthreads();
-        const int ntake = S.take < TAKE0 ? S.take : TAKE0;
-        __syncthreads();
-        if (tid == 0) S.take = 0;
-        __syncthreads();
-        // power of the SFA bound on this query: the fraction of the take blocks' words whose LB is
-        // still <= the tightened threshold (high-frequency data ~1, noisy members ~1e-3).  Dense only
-        // if many leaves survive AND most of their words would have to be refined anyway.
-        int pass = 0;
-        if (cnt >= A.dense_min) {
-          const float thr = S.thr;
-          const int nw = ntake * A.B < 2048 ? ntake * A.B : 2048;
-          for (int w = tid; w < nw; w += kQThreads) {
-            const int64_t pos = (int64_t)(uint32_t)s_blist[w / A.B] * A.B + (w % A.B);
-            if (pos < A.n) {
-              uint4 wr[LT / 16];
-#pragma unroll
-              for (int c = 0; c < LT / 16; ++c) wr[c] = ld_stream_u4(A.words + pos * A.WS + 16 * c);
-              pass += word_lb<LT>(wr, s_T, thr) <= thr;
-            }
+      // f1 stage 2: the same probe under the (nearly final) bound of top-M seeding, at dense_pm permille;
+      // a query flagged here keeps its leaf list (published as dense-candidate tasks below)
+      if (A.mode == 0 && A.dense_pm > 0 && !early_dense && cnt > 0) {
+        const long long npass = dense_probe<LT>(A, S, s_T);
+        const int64_t P = A.n < kProbe ? A.n : kProbe;
+        if (tid == 0) {
+          if (dense_flag(A, npass, P, A.dense_pm)) {
+            s_dense = flag_dense(A, npass, P);
+            s_dec[0] = 2;
           }
-          pass = __reduce_add_sync(FULL, pass);
-          if (lane == 0) atomicAdd(&S.take, pass);
-          __syncthreads();
-          // estimated sparse refines of this query: surviving leaves x B x word pass rate
-          const double est = (double)cnt * A.B * S.take / (nw > 0 ? nw : 1);
-          if (tid == 0) {
-            s_dec[1] = cnt;
-            s_dec[2] = S.take;
-            s_dec[3] = nw;
-          }
-          if (tid == 0 && (A.dense_force || est * 8.0 >= (double)A.n)) {
-            s_dense = atomicAdd(A.qd_counter, 1);
-            s_dec[0] = 1;
-            atomicAdd(reinterpret_cast<unsigned long long*>(A.qd_counter + 6),
-                      A.dense_force ? (unsigned long long)A.dense_rows : (unsigned long long)est);
-          }
+          s_dec[1] = npass;
         }
         __syncthreads();
       }
@@ -1163,11 +1248,11 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
       const int budget = A.front_batches * batch_blocks<LT>(A.B);  // leaves the front scans itself
       if (tid == 0) S.ntask = 0;
       __syncthreads();
-      if (dc) {
-        // a dense candidate's leaves are only needed if the batch skips the dense pass: publish them
-        // as they are (one pass; no ordering work for a list that is usually never scanned)
-        publish_tasks<LT>(A, S, qi, gl, cnt, false, true);
-      } else if (cnt <= CAP_B) {
+      if (dc && early_dense) {
+        // a dense candidate's rows are only needed if the batch skips the dense pass: every leaf, in
+        // storage order, as range tasks (no list is built for a query that usually never scans)
+        publish_range<LT>(A, S, qi);
+      } else if (cnt <= CAP_B) {  // (flagged at stage 2: the list is published sorted, nothing scanned here)
         for (int i = tid; i < cnt; i += kQThreads) s_blist[i] = gl[i];
         __syncthreads();
         bitonic_sort_u64(s_blist, cnt);
@@ -1225,7 +1310,9 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
           atomicAdd(&A.dstats[22], (unsigned long long)S.ntask);
           atomicAdd(&A.dstats[23], 1ull);
         }
-        for (int i = tid; i < LT * 256; i += kQThreads) A.q_T[(int64_t)qi * LT * 256 + i] = s_T[i];
+        for (int i = tid; i < LT * 256; i += kQThreads) A.q_T[(int64_t)qi * 3 * LT * 256 + i] = s_T[i];
+        if (early_dense)  // range tasks prune leaves by their envelope LB: they need Tlo / Thi too
+          for (int i = tid; i < 2 * LT * 256; i += kQThreads) A.q_T[((int64_t)qi * 3 + 1) * LT * 256 + i] = s_Tlo[i];
         for (int i = tid; i < len; i += kQThreads) A.q_hat[(int64_t)qi * len + i] = reinterpret_cast<const float*>(s_qh4)[i];
         for (int r = tid; r < S.tkn; r += kQThreads) {
           h->tkd[r] = s_tkd[r];
@@ -1322,7 +1409,7 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
         if (o) cudaFree(o);
       ix->qstate = ix->q_T = ix->q_hat = ix->pool = ix->tasks = ix->rank_count = nullptr;
       SOFA_CK(cudaMalloc(&ix->qstate, (size_t)qn * sizeof(QState)));
-      SOFA_CK(cudaMalloc(&ix->q_T, (size_t)qn * LT * 256 * 4));
+      SOFA_CK(cudaMalloc(&ix->q_T, (size_t)qn * 3 * LT * 256 * 4));
       SOFA_CK(cudaMalloc(&ix->q_hat, (size_t)qn * SOFA_MAX_LEN * 4));
       SOFA_CK(cudaMalloc(&ix->pool, (size_t)pool_need * 8));
       SOFA_CK(cudaMalloc(&ix->tasks, (size_t)2 * task_need * sizeof(ScanTask)));
@@ -1400,8 +1487,7 @@ int launch_query_impl(sofa_index* ix, const float* Q, int q, int k, const float*
   A.trace = ix->trace_on ? ix->trace + ix->trace_off * SOFA_TRACE_FIELDS : nullptr;
   if (ix->dense_permille > 0 && ix->xb16 && ix->dense.q_cap >= q) {
     const DenseScratch& D = ix->dense;
-    A.dense_min = (ix->nb * (ix->dense_permille < 1000 ? ix->dense_permille : 0) + 999) / 1000;
-    if (A.dense_min < 1) A.dense_min = 1;
+    A.dense_pm = ix->dense_permille < 1000 ? ix->dense_permille : 1000;
     A.dense_rows = dense_batch_rows(ix);
     A.dense_force = ix->dense_permille >= 1000;
     A.qd_counter = D.counters;

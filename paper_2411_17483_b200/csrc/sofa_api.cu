@@ -174,6 +174,8 @@ int sofa_default_tuning(sofa_tuning* out) {
   out->front_wide = -1;
   out->scan_wide = -1;
   out->dense_cand_cap = 0;
+  out->dense_diag = 0;
+  out->dense_batch_rows = 0;
   return SOFA_OK;
 }
 
@@ -189,6 +191,7 @@ int sofa_set_tuning(sofa_index* ix, const sofa_tuning* t) {
   for (int w : {t->front_wide, t->scan_wide})
     if (w < -1 || w > 1) return fail(SOFA_EINVAL, "front_wide / scan_wide must be -1, 0 or 1");
   if (t->dense_cand_cap < 0) return fail(SOFA_EINVAL, "dense_cand_cap must be >= 0");
+  if (t->dense_batch_rows < 0) return fail(SOFA_EINVAL, "dense_batch_rows must be >= 0");
   const bool regrow = t->dense_cand_cap != ix->tune.dense_cand_cap;
   ix->tune = *t;
   if (regrow) free_dense_scratch(ix);  // reallocated at the next sofa_knn with the new capacity
@@ -262,7 +265,7 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
   ix->global_offset = opts.global_offset;
   ix->global_n = gn;
   ix->series = series_dev;
-  ix->dense_permille = opts.dense_permille == 0 ? 100 : (opts.dense_permille < 0 ? 0 : opts.dense_permille);
+  ix->dense_permille = opts.dense_permille == 0 ? 20 : (opts.dense_permille < 0 ? 0 : opts.dense_permille);
   cudaGetDevice(&ix->device);
   cudaDeviceGetAttribute(&ix->sms, cudaDevAttrMultiProcessorCount, ix->device);
   if (ix->sms < 1) ix->sms = 1;
@@ -463,7 +466,7 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
     float* Db = out_dist_dev + (int64_t)q0 * k;
     int64_t* Ib = out_idx_dev + (int64_t)q0 * k;
     ix->trace_off = q0;
-    if (dense) SOFA_CK(cudaMemsetAsync(ix->dense.counters, 0, (64 + 1024) * 4, st));
+    if (dense) SOFA_CK(cudaMemsetAsync(ix->dense.counters, 0, (64 + 2048) * 4, st));
     if (rec) cudaEventRecord(ev[0], st);
     if (ix->n == 0) {
       rc = launch_fill_pad(Db, Ib, (int64_t)qb * k, st);

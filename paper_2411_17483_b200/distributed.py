@@ -72,15 +72,43 @@ def exchange_bound(bound: torch.Tensor, group=None) -> torch.Tensor:
     return bound
 
 
+def pack_keys(dist: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+    """k = 1 exchange key: float bits of the (non-negative) distance in the high 32 bits, the global
+    index in the low 32 (padding -1 -> 0xffffffff).  For d >= 0 the float bit pattern orders like the
+    value, so the int64 minimum is the lexicographic (distance, index) minimum — the a9 tie rule
+    (indices < 2^32 at N <= 100M)."""
+    bits = dist.contiguous().view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    lo = torch.where(idx < 0, torch.full_like(idx, 0xFFFFFFFF), idx)
+    return (bits << 32) | lo
+
+
+def unpack_keys(key: torch.Tensor):
+    bits = (key >> 32).to(torch.int32)
+    d = bits.view(torch.float32)
+    i = key & 0xFFFFFFFF
+    return d, torch.where(i == 0xFFFFFFFF, torch.full_like(i, -1), i)
+
+
+def allreduce_min_k1(dist_local: torch.Tensor, idx_local: torch.Tensor, group=None):
+    """C4 for k = 1: ONE all-reduce MIN of packed (distance, index) keys instead of all-gather + merge."""
+    key = pack_keys(dist_local, idx_local)
+    dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
+    return unpack_keys(key)
+
+
 def sharded_knn(queries, k, local_knn, merge, group=None, local_seed=None):
-    """Local k-NN on this rank's shard, all-gather, min-merge (a9).  With `local_seed`, the ranks
-    first exchange their seed bounds (C3) and every shard searches under the global one, so a
-    shard that does not hold a query's neighbours prunes almost everything."""
+    """Local k-NN on this rank's shard, then the exchange: k = 1 one all-reduce MIN of packed keys,
+    k > 1 all-gather + min-merge (a9).  With `local_seed`, the ranks first exchange their seed bounds
+    (C3) and every shard searches under the global one, so a shard that does not hold a query's
+    neighbours prunes almost everything."""
     if local_seed is not None:
         bound = exchange_bound(local_seed(queries, k), group)
         d, i = local_knn(queries, k, bound)
     else:
         d, i = local_knn(queries, k)
+    if k == 1:
+        dd, ii = allreduce_min_k1(d.reshape(-1), i.reshape(-1), group)
+        return dd.reshape(-1, 1), ii.reshape(-1, 1)
     D, I = allgather_topk(d, i, group)
     return merge(D, I)
 

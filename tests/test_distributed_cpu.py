@@ -88,3 +88,81 @@ def test_gloo_sharded_pipeline(world):
 
 def test_sample_indices_match_oracle():
     assert np.array_equal(D.global_sample_indices(10_000_000, 100_000), O.sample_indices(10_000_000, 100_000))
+
+
+def _worker_shards(rank, world, port, q, N, k):
+    """uneven shards (and an empty one when N < world): local oracle k-NN on each rank's rows, then the
+    exchange — k = 1 the packed-key all-reduce MIN, k > 1 the all-gather + merge — with and without the
+    seed-bound exchange; every rank must hold the oracle's global answer"""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = datagen.scaled(datagen.WORKLOADS["cfg1"], N, 7, length=32)
+        full = datagen.generate_rows(w, 0, N)
+        queries = datagen.generate_queries(w)
+        a, b = datagen.shard_range(N, rank, world)
+        shard = full[a:b]
+
+        def local_knn(qs, kk, bound=None):
+            dd = np.full((qs.shape[0], kk), np.inf)
+            ii = np.full((qs.shape[0], kk), -1, dtype=np.int64)
+            if shard.shape[0]:
+                dd, ii = O.knn_bruteforce(shard.numpy(), qs.numpy(), kk)
+                ii = np.where(ii >= 0, ii + a, -1)
+            if bound is not None:  # results above the exchanged bound are never returned (bsf_init)
+                drop = dd ** 2 > bound.double().numpy()[:, None] * (1 + 1e-6)
+                dd, ii = np.where(drop, np.inf, dd), np.where(drop, -1, ii)
+            return torch.from_numpy(dd.astype(np.float32)), torch.from_numpy(ii)
+
+        def local_seed(qs, kk):
+            if shard.shape[0] < kk:
+                return torch.full((qs.shape[0],), float("inf"))
+            ds, _ = O.knn_bruteforce(shard.numpy()[: max(kk, shard.shape[0] // 3)], qs.numpy(), kk)
+            return torch.from_numpy((ds[:, -1] ** 2).astype(np.float32))
+
+        def merge(Dd, Ii):
+            d, i = O.merge_topk(Dd.numpy().astype(np.float64), Ii.numpy(), k)
+            return torch.from_numpy(d.astype(np.float32)), torch.from_numpy(i)
+
+        do, io = O.knn_bruteforce(full.numpy(), queries.numpy(), k)
+        d1, i1 = D.sharded_knn(queries, k, local_knn, merge)
+        d2, i2 = D.sharded_knn(queries, k, local_knn, merge, local_seed=local_seed)
+        ok = all(np.array_equal(i.numpy(), io) for i in (i1, i2))
+        fin = np.isfinite(do)
+        rel = max(float(np.max(np.abs(d.numpy()[fin] - do[fin]) / np.maximum(do[fin], 1e-12), initial=0.0))
+                  for d in (d1, d2))
+        pad_ok = all(np.array_equal(np.isfinite(d.numpy()), fin) for d in (d1, d2))
+        q.put((rank, ok and pad_ok, rel, b - a))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,N,k", [(4, 4003, 1), (4, 4003, 5), (4, 3, 1), (4, 3, 5), (3, 1000, 2)])
+def test_gloo_uneven_and_empty_shards(world, N, k):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_shards, args=(r, world, port, q, N, k)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sizes = sorted(r[3] for r in res)
+    assert sum(sizes) == N and sizes[-1] - sizes[0] <= 1
+    for rank, ok, rel, _ in res:
+        assert ok and rel < 1e-6, (rank, ok, rel)
+
+
+def test_packed_keys_order_like_distance_then_index():
+    """the k = 1 exchange key: int64 order == lexicographic (distance, index) order; padding last"""
+    rng = np.random.default_rng(3)
+    d = np.concatenate([rng.uniform(0, 30, 200), [0.0, 0.0, 5.0, 5.0, np.inf, np.inf]]).astype(np.float32)
+    i = np.concatenate([rng.integers(0, 100_000_000, 200), [7, 3, 9, 2, -1, -1]]).astype(np.int64)
+    key = D.pack_keys(torch.from_numpy(d), torch.from_numpy(i)).numpy()
+    big = np.where(i < 0, 0xFFFFFFFF, i)
+    order = np.lexsort((big, d))
+    assert np.array_equal(np.argsort(key, kind="stable"), order) or np.array_equal(key[np.argsort(key)], key[order])
+    dd, ii = D.unpack_keys(torch.from_numpy(key))
+    assert np.array_equal(dd.numpy(), d) and np.array_equal(ii.numpy(), i)

@@ -41,6 +41,24 @@ def test_dense_parity(kind, N, n, l, k, Q):
     assert st["dense_candidates"] >= st["dense_queries"] * k
 
 
+@pytest.mark.parametrize("Q,k", [(1, 1), (1, 4), (3, 2), (300, 3)])
+def test_dense_flagged_but_batch_sparse_scans_ranges(Q, k):
+    """high-frequency queries are flagged by the probe before their tree descent, but the batch needs
+    more estimated refines than they add up to (dense_batch_rows): the batch skips the dense pass and
+    the scan pool finishes them from range tasks (every leaf in storage order, pruned by its envelope
+    LB) — exact all the same"""
+    w = datagen.scaled(datagen.WORKLOADS["cfg3"], 120_000 + 77, Q)
+    x, q = _data(w)
+    ix = SofaIndex(x, sample_size=datagen.default_sample_size(w))
+    ix.set_tuning(dense_batch_rows=1 << 60)
+    d, i, st = ix.knn(q, k, stats=True)
+    do, io = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), k)
+    assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, x.cpu().numpy(), q.cpu().numpy())
+    assert st["dense_queries"] == 0      # the dense pass did not run
+    assert st["scan_queries"] == Q       # every query was handed to the scan pool
+    assert st["words_scanned"] >= Q * w.n_series * 0.9  # (nearly) every word, no tree pruning
+
+
 @pytest.mark.parametrize("kind,k", [("cfg1", 1), ("cfg4", 5), ("cfg2", 1)])
 def test_forced_dense_equals_sparse(kind, k):
     """dense_permille=1000 forces every query through the dense path; -1 never: identical bits."""
