@@ -85,12 +85,12 @@ typedef struct {
   int32_t dense_permille;  /* dense path: a strided probe of 2048 stored words
                               estimates the fraction of rows the sparse path would refine.  A query
                               is flagged before its envelope-tree descent if >= 10% of the probe
-                              passes the bound of its own-key seed, else after top-M seeding if >=
-                              this many permille pass the tightened bound (and the estimate is >=
-                              4096 rows either way).  The batch runs the tensor-core pass only if
+                              passes the bound of its own-key seed, else — once the batch's dense
+                              pass is certain — after top-M seeding if >= this many permille pass
+                              the tightened bound (and the estimate is >= 4096 rows either way).  The batch runs the tensor-core pass only if
                               the flagged queries' estimated refines add up to one pass over the
                               rows (sofa_tuning.dense_batch_rows); else the scan pool finishes them
-                              sparsely.  0 => 20 (2%), < 0 => never, >= 1000 => every query
+                              sparsely.  0 => 5 (0.5%), < 0 => never, >= 1000 => every query
                               (testing).  Results are identical either way; only speed changes. */
   int64_t global_offset;   /* global index of this shard's row 0 (0 on one GPU) */
   int64_t global_n;        /* total rows over all shards (0 => this call's n) */
@@ -249,7 +249,8 @@ int sofa_transform(const float* series_dev, int64_t n, const sofa_model* model, 
 
 /* Index introspection: number of rows / blocks / block size / word stride, and the GPU time of the
  * build phases (CUDA events on the build stream; the analog of Fig. 7): model (sample +
- * learning, a2), transform (a1 + a3), sort (a4 key sort), gather + envelopes (a4). */
+ * learning, a2, plus the index allocations), transform (a1 + a3), sort (a4 key sort), gather +
+ * envelopes (a4). */
 typedef struct {
   int64_t n, n_blocks, global_offset, global_n;
   int32_t len, l, alphabet, block_size, word_stride;
@@ -285,12 +286,13 @@ const char* sofa_last_error(void);
 int64_t sofa_launch_count(void);
 
 /* Live per-kernel timing of sofa_knn calls without stats (bench.py's roofline, measured over its
- * timed region).  While enabled, every sofa_knn sub-batch records four CUDA events on the call's
- * stream (before the front, after it, after the dense pass, after the scan) and nothing else: no
- * synchronisation, no counters.  Each call to this function first drains the recorded events
- * (blocking until the last recorded sub-batch has finished), adds their elapsed times to the
- * totals and, if out_ms / out_groups are non-NULL, writes the totals: out_ms[3] = summed GPU ms of
- * the front, dense and scan launch groups, *out_groups = sub-batches timed.  Then enable = 1 clears
+ * timed region).  While enabled, every sofa_knn sub-batch records five CUDA events on the call's
+ * stream (before the front, after it, after the dense screen, after the dense refine, after the
+ * scan) and nothing else: no synchronisation, no counters.  Each call to this function first drains
+ * the recorded events (blocking until the last recorded sub-batch has finished), adds their elapsed
+ * times to the totals and, if out_ms / out_groups are non-NULL, writes the totals: out_ms[4] =
+ * summed GPU ms of the front, the dense screen, the dense exact refine and the scan launch groups,
+ * *out_groups = sub-batches timed.  Then enable = 1 clears
  * the totals and starts timing, 0 clears them and stops, -1 leaves the state unchanged (read only).
  * Errors: SOFA_EINVAL for a NULL index; CUDA errors as SOFA_ECUDA. */
 int sofa_kernel_timing(sofa_index* ix, int32_t enable, double* out_ms, int64_t* out_groups);

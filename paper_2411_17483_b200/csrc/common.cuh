@@ -283,7 +283,7 @@ struct sofa_index {
   float2* stats_orig = nullptr;   // n, original row order (dense path)
   __nv_bfloat16* xb16 = nullptr;  // n x xb_ld, original row order: z-normalised rows in bfloat16 (dense screen)
   int xb_ld = 0;                  // row stride of xb16 (len rounded up to 8: 16-byte TMA rows)
-  int32_t dense_permille = 20;    // dense path when >= this many permille of probed words pass (0: off)
+  int32_t dense_permille = 5;     // dense path when >= this many permille of probed words pass (0: off)
   double build_ms[4] = {};        // model, transform, sort, gather + envelopes (CUDA events)
   DenseScratch dense;
   int32_t* perm = nullptr;        // n: sorted position -> local row
@@ -310,8 +310,8 @@ struct sofa_index {
   int trace_on = 0;
   // live per-launch-group timing (sofa_kernel_timing): 4 events per sub-batch, read back lazily
   int ktime_on = 0;
-  std::vector<std::array<cudaEvent_t, 4>> ktime_pending, ktime_free;
-  double ktime_ms[3] = {0, 0, 0};
+  std::vector<std::array<cudaEvent_t, 5>> ktime_pending, ktime_free;
+  double ktime_ms[4] = {0, 0, 0, 0};
   int64_t ktime_groups = 0;
   int64_t trace_off = 0;  // first query row of the current sub-batch in the trace
   int32_t trace_q = 0;
@@ -349,7 +349,8 @@ int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_
 inline int64_t dense_batch_rows(const sofa_index* ix) {
   return ix->tune.dense_batch_rows > 0 ? ix->tune.dense_batch_rows : (ix->n > 0 ? ix->n : 1);
 }
-int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stats, cudaStream_t st);
+int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stats, cudaStream_t st,
+                 cudaEvent_t after_screen = nullptr);
 int ensure_dense_scratch(sofa_index* ix, int q, int k);
 int dense_dots(const float* rows, int64_t m, int len, const float* queries, int q, float* out, cudaStream_t st);
 void free_dense_scratch(sofa_index* ix);

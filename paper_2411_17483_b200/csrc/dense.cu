@@ -807,7 +807,8 @@ static void fill_screen_args(sofa_index* ix, int k, DenseArgs& A) {
   A.diag = ix->tune.dense_diag;
 }
 
-int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stats, cudaStream_t st) {
+int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stats, cudaStream_t st,
+                 cudaEvent_t after_screen) {
   DenseScratch& D = ix->dense;
   int rc;
   if (D.tmap_q_rows != q) {  // tensor maps are encoded once per buffer (not on every call)
@@ -822,6 +823,7 @@ int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stat
                           *reinterpret_cast<const CUtensorMap*>(D.tmap_q), A, D_SMEM_MAX,
                           st)))
     return rc;
+  if (after_screen) cudaEventRecord(after_screen, st);
 
   DensePost P{};
   P.series = ix->series;

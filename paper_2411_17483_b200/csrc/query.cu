@@ -1185,9 +1185,18 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
         gl2 = t;
       }
       t_sub[0] = clock64();  // top-M seeding done
-      // f1 stage 2: the same probe under the (nearly final) bound of top-M seeding, at dense_pm permille;
-      // a query flagged here keeps its leaf list (published as dense-candidate tasks below)
-      if (A.mode == 0 && A.dense_pm > 0 && !early_dense && cnt > 0) {
+      // f1 stage 2: the same probe under the (nearly final) bound of top-M seeding, at dense_pm permille —
+      // only once the batch's dense pass is certain (the flagged estimates already add up to dense_rows;
+      // the sum only grows), so a query flagged here never falls back to the scan pool's dense-candidate
+      // set, and a batch without a dense pass keeps every query on the ordinary sparse path
+      // (read once by thread 0: the counter moves, and the branch below must be block-uniform)
+      if (tid == 0)
+        S.take = A.qd_counter && *reinterpret_cast<volatile unsigned long long*>(A.qd_counter + 6) >=
+                                     (unsigned long long)A.dense_rows;
+      __syncthreads();
+      const bool batch_dense = S.take != 0;
+      __syncthreads();
+      if (A.mode == 0 && A.dense_pm > 0 && !early_dense && cnt > 0 && batch_dense) {
         const long long npass = dense_probe<LT>(A, S, s_T);
         const int64_t P = A.n < kProbe ? A.n : kProbe;
         if (tid == 0) {
@@ -1252,7 +1261,9 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
         // a dense candidate's rows are only needed if the batch skips the dense pass: every leaf, in
         // storage order, as range tasks (no list is built for a query that usually never scans)
         publish_range<LT>(A, S, qi);
-      } else if (cnt <= CAP_B) {  // (flagged at stage 2: the list is published sorted, nothing scanned here)
+      } else if (dc) {
+        // flagged at stage 2, when the batch's dense pass was already certain: nothing to publish
+      } else if (cnt <= CAP_B) {
         for (int i = tid; i < cnt; i += kQThreads) s_blist[i] = gl[i];
         __syncthreads();
         bitonic_sort_u64(s_blist, cnt);

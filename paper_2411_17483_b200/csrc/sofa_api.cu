@@ -140,9 +140,9 @@ int sofa_kernel_timing(sofa_index* ix, int32_t enable, double* out_ms, int64_t* 
   g_err.clear();
   if (!ix) return fail(SOFA_EINVAL, "index is NULL");
   // drain what was recorded so far: blocks until the last recorded group has finished
-  if (!ix->ktime_pending.empty()) SOFA_CK(cudaEventSynchronize(ix->ktime_pending.back()[3]));
+  if (!ix->ktime_pending.empty()) SOFA_CK(cudaEventSynchronize(ix->ktime_pending.back()[4]));
   for (auto& quad : ix->ktime_pending) {
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 4; ++i) {
       float ms = 0.f;
       SOFA_CK(cudaEventElapsedTime(&ms, quad[i], quad[i + 1]));
       ix->ktime_ms[i] += ms;
@@ -152,7 +152,7 @@ int sofa_kernel_timing(sofa_index* ix, int32_t enable, double* out_ms, int64_t* 
   }
   ix->ktime_pending.clear();
   if (out_ms)
-    for (int i = 0; i < 3; ++i) out_ms[i] = ix->ktime_ms[i];
+    for (int i = 0; i < 4; ++i) out_ms[i] = ix->ktime_ms[i];
   if (out_groups) *out_groups = ix->ktime_groups;
   if (enable >= 0) {  // (re)start: clear the totals
     ix->ktime_on = enable != 0;
@@ -265,7 +265,7 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
   ix->global_offset = opts.global_offset;
   ix->global_n = gn;
   ix->series = series_dev;
-  ix->dense_permille = opts.dense_permille == 0 ? 20 : (opts.dense_permille < 0 ? 0 : opts.dense_permille);
+  ix->dense_permille = opts.dense_permille == 0 ? 5 : (opts.dense_permille < 0 ? 0 : opts.dense_permille);
   cudaGetDevice(&ix->device);
   cudaDeviceGetAttribute(&ix->sms, cudaDevAttrMultiProcessorCount, ix->device);
   if (ix->sms < 1) ix->sms = 1;
@@ -316,7 +316,6 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
     if (rc) return bail(rc);
   }
   if ((rc = upload_model(ix->model, len, ix, st))) return bail(rc);
-  cudaEventRecord(ev.e[1], st);
   const int WS = ix->WS, B = ix->B;
   ix->nb = (n + B - 1) / B;
   if (cudaMalloc(&ix->qcounter, 64) != cudaSuccess || cudaMalloc(&ix->dstats, 32 * 8) != cudaSuccess)
@@ -378,6 +377,8 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
       ix->dense_permille = 0;
     }
   }
+  // (the model phase ends here: it includes the index allocations above, which are host-synchronous)
+  cudaEventRecord(ev.e[1], st);
   if ((rc = launch_transform(series_dev, n, ix->dm, ix->model, words_u, stats_u, keys_u, nullptr, nullptr, ix->xb16,
                              st))) {
     freeall();
@@ -441,23 +442,23 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
   // pool holds one leaf list per query: q x ceil(n/B) entries)
   const int qb_max = q < kQueryBatch ? q : kQueryBatch;
   if (dense && (rc = ensure_dense_scratch(ix, qb_max, k))) return rc;
-  // with stats: CUDA events on `st` around each launch group (front, dense pass, scan)
-  cudaEvent_t ev[4] = {};
+  // with stats: CUDA events on `st` around each launch group (front, dense screen, dense refine, scan)
+  cudaEvent_t ev[5] = {};
   if (stats)
     for (auto& e : ev) SOFA_CK(cudaEventCreate(&e));
-  double kms[3] = {0, 0, 0};
+  double kms[4] = {0, 0, 0, 0};
   rc = SOFA_OK;
   for (int q0 = 0; q0 < q && !rc; q0 += qb_max) {
-    // live timing (sofa_kernel_timing): the same four points, recorded without synchronising
+    // live timing (sofa_kernel_timing): the same five points, recorded without synchronising
     if (!stats && ix->ktime_on) {
       if (ix->ktime_free.empty()) {
-        std::array<cudaEvent_t, 4> quad{};
+        std::array<cudaEvent_t, 5> quad{};
         for (auto& e : quad) SOFA_CK(cudaEventCreate(&e));
         ix->ktime_free.push_back(quad);
       }
       ix->ktime_pending.push_back(ix->ktime_free.back());
       ix->ktime_free.pop_back();
-      for (int i = 0; i < 4; ++i) ev[i] = ix->ktime_pending.back()[i];
+      for (int i = 0; i < 5; ++i) ev[i] = ix->ktime_pending.back()[i];
     }
     const bool rec = stats || ix->ktime_on;
     const int qb = q - q0 < qb_max ? q - q0 : qb_max;
@@ -473,6 +474,7 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
       if (rec) {
         cudaEventRecord(ev[1], st);
         cudaEventRecord(ev[2], st);
+        cudaEventRecord(ev[3], st);
       }
     } else {
       // front (per query) -> dense pass for flagged queries if the batch warrants it -> scan tasks
@@ -480,14 +482,15 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
       // the batch decision from device counters, so there is no host synchronisation in between
       rc = launch_query(ix, Qb, qb, k, Bb, Db, Ib, st, false);
       if (rec) cudaEventRecord(ev[1], st);
-      if (!rc && dense) rc = launch_dense(ix, qb, k, Db, Ib, stats != nullptr, st);
-      if (rec) cudaEventRecord(ev[2], st);
+      if (!rc && dense) rc = launch_dense(ix, qb, k, Db, Ib, stats != nullptr, st, rec ? ev[2] : nullptr);
+      else if (rec) cudaEventRecord(ev[2], st);
+      if (rec) cudaEventRecord(ev[3], st);
       if (!rc) rc = launch_query(ix, Qb, qb, k, Bb, Db, Ib, st, true);
     }
-    if (rec) cudaEventRecord(ev[3], st);
+    if (rec) cudaEventRecord(ev[4], st);
     if (stats) {
-      cudaEventSynchronize(ev[3]);
-      for (int i = 0; i < 3; ++i) {
+      cudaEventSynchronize(ev[4]);
+      for (int i = 0; i < 4; ++i) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
         kms[i] += ms;
@@ -523,7 +526,9 @@ int sofa_knn(sofa_index* ix, const float* queries_dev, int32_t q, int32_t k, con
     stats->dense_refined = (int64_t)h[21];
     stats->scan_tasks = (int64_t)h[22];
     stats->scan_queries = (int64_t)h[23];
-    for (int i = 0; i < 3; ++i) stats->kernel_ms[i] = kms[i];
+    stats->kernel_ms[0] = kms[0];
+    stats->kernel_ms[1] = kms[1] + kms[2];  // the dense pass: screen + exact refine
+    stats->kernel_ms[2] = kms[3];
   }
   return SOFA_OK;
 }

@@ -149,10 +149,12 @@ def sofa_launch_count() -> int:
 def sofa_kernel_timing(ix: int, enable: int) -> tuple[dict, int]:
     """drain the live timing events; returns ({front, dense, scan} summed ms, sub-batches timed) and
     then enables (1), disables (0) or keeps (-1) timing; see include/sofa.h"""
-    ms = (C.c_double * 3)()
+    ms = (C.c_double * 4)()
     groups = I64(0)
     _ck(lib().sofa_kernel_timing(ix, enable, ms, C.byref(groups)))
-    return dict(zip(("front", "dense", "scan"), map(float, ms))), int(groups.value)
+    front, screen, post, scan = map(float, ms)
+    return {"front": front, "dense": screen + post, "scan": scan, "dense_screen": screen, "dense_post": post}, \
+        int(groups.value)
 
 
 def sofa_default_opts() -> sofa_build_opts:

@@ -313,7 +313,9 @@ def test_large_batch_runs_in_sub_batches():
     km, groups = ix.kernel_timing(0)
     assert groups == 3 + 1 and km["front"] > 0 and km["scan"] > 0 and km["dense"] >= 0
     assert torch.equal(i2, i) and torch.equal(d2, d) and torch.equal(i3, i[:10])
-    assert ix.kernel_timing(-1) == ({"front": 0.0, "dense": 0.0, "scan": 0.0}, 0)  # stopped and cleared
+    km0, g0 = ix.kernel_timing(-1)  # stopped and cleared
+    assert g0 == 0 and set(km0) == {"front", "dense", "scan", "dense_screen", "dense_post"} and not any(km0.values())
+    assert abs(km["dense"] - km["dense_screen"] - km["dense_post"]) < 1e-9
     ix.knn(q[:10].contiguous(), 3)
     assert ix.kernel_timing(-1)[1] == 0
 
