@@ -145,6 +145,10 @@ typedef struct {
   int64_t dense_batch_rows; /* the batch runs the dense pass iff its flagged queries' estimated sparse
                               refines add up to at least this many rows (0 => n, one pass over the
                               rows); a batch below it scans its flagged queries sparsely */
+  int32_t dense_pair;      /* dense screen on CTA pairs (tcgen05 cta_group::2, M = 256 rows per MMA, each
+                              SM holding half of the query operand) instead of single CTAs (M = 128),
+                              for rows of n <= 512 (default 0: measured equal on configs[3] and slower
+                              on configs[2]) */
   int32_t dense_diag;      /* TIMING DIAGNOSTIC ONLY, 0 in any real use: nonzero bits make the dense
                               screen skip work so its pipeline stages can be timed apart (results are
                               then WRONG): 1 = no screening math, 2 = no TMEM loads either,

@@ -259,6 +259,7 @@ struct DenseScratch {
   float* tkd = nullptr;            // slot x k_cap
   int* tki = nullptr;              // slot x k_cap (local rows)
   int* tkn = nullptr;
+  unsigned long long* key1 = nullptr;  // slot: k = 1 best as (d^2 bits << 32 | local row), lock-free min
   int* lock = nullptr;
   float* ubl = nullptr;            // slot x k_cap: k smallest upper bounds of candidate rows (k > 1)
   int* ubn = nullptr;
@@ -330,7 +331,7 @@ namespace sofa {
 int upload_model(const sofa_model& m, int len, sofa_index* ix, cudaStream_t st);
 int launch_transform(const float* X, int64_t N, const DevModel& dm, const sofa_model& m, uint8_t* words,
                      float2* stats, uint64_t* keys, double* vals, uint8_t* words_l, __nv_bfloat16* xb16,
-                     cudaStream_t st);
+                     cudaStream_t st, cudaEvent_t t_start = nullptr);
 int launch_envelopes(const uint8_t* words, int64_t n, int B, int WS, const uint64_t* skeys, uint8_t* env,
                      uint64_t* bkey, cudaStream_t st);
 int launch_env_up(const uint8_t* child, int64_t nchild, int WS, uint8_t* parent, cudaStream_t st);

@@ -48,7 +48,7 @@ constexpr int DA_BYTES = DM * DKC * 2;   // 16 KB per A stage
 constexpr int D_THREADS = 352;           // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2..9 epilogue (2 groups),
                                          // warp 10 threshold refresher
 constexpr int D_AHEAD = 8;               // row tiles a CTA may run ahead of its twins
-constexpr int D_MAX_STAGES = 8;          // A ring depth cap (barrier arrays)
+constexpr int D_MAX_STAGES = 12;         // A ring depth cap (barrier arrays)
 constexpr int D_SMEM_MAX = 232448 - 2048;  // opt-in shared memory per CTA on sm_100, less the static part
 constexpr int D_MISC = 4096;             // per-query thresholds / norms + barriers
 
@@ -96,6 +96,47 @@ __device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t adesc, uin
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// ---- CTA-pair (cta_group::2) variants: every tcgen05 instruction of a kernel uses the same cta_group
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// the shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// 2-SM TMA: the data lands in this CTA's shared memory, the transaction bytes count on the barrier at
+// `bar_cluster` (the leader CTA's)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int x, int y, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* b) {  // arrive on the barrier in both CTAs of the pair
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(b)),
+               "h"((uint16_t)3)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_bf16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row atoms 1024 B apart (SBO),
 // LBO unused for swizzled K-major (1), version 1 (sm_100), base offset 0 (1024-aligned tiles).
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
@@ -104,8 +145,8 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
 }
 // instruction descriptor, kind::f16: D f32 (bits 4-5 = 1), A/B bf16 (bits 7-9, 10-12 = 1), both
 // K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28 (cute/arch/mma_sm100_desc.hpp layout)
-__device__ __forceinline__ uint32_t idesc_bf16(int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(DM >> 4) << 24);
+__device__ __forceinline__ uint32_t idesc_bf16(int n, int m = DM) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 #define TMEM_LD32(addr, r)                                                                                        \
@@ -135,6 +176,7 @@ struct DenseArgs {
   int64_t cand_cap;  // split into one slice per CTA (cand_cap / gridDim.x entries each)
   int* slice_count;  // per CTA: candidates emitted (may exceed the slice: overflow)
   int streamed;      // STR mode (queries streamed with the rows; n = 1024) vs RES (queries resident)
+  int pair;          // RES on CTA pairs (tcgen05 cta_group::2, M = 256; sofa_tuning.dense_pair)
   int* overflow;  // per slot flag
   int* ovf_list;
   int* ovf_count;
@@ -263,6 +305,12 @@ __device__ void emit_chunk(const DenseArgs& A, uint32_t m, const uint32_t (&v)[3
 // units (b / g) + j c; CTAs b >= c g idle.  "Twins": CTAs with the same b / g (same units).  A unit is
 // one row tile with the group's queries resident in shared memory (RES: rows n <= 512), or two row
 // tiles sharing the query chunks streamed next to them (STR: the queries do not fit, n = 1024).
+// PAIR (RES only): clusters of 2 CTAs on one TPC run M = 256 MMAs (tcgen05 cta_group::2, issued by the
+// leader): a unit is 256 rows, each CTA streams its 128 and holds HALF of the group's queries, so each
+// SM's shared memory feeds half the query operand (the single-CTA M = 128 MMA at N = 176 needs more
+// shared-memory bandwidth than the SM has, next to the TMA fills); each CTA's TMEM holds its 128 rows
+// x all N columns, read by its own epilogue.
+template <bool PAIR>
 __global__ void __launch_bounds__(D_THREADS, 1)
     k_dense_screen(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const DenseArgs A) {
   extern __shared__ __align__(1024) unsigned char dsm_raw[];
@@ -278,23 +326,27 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   if (!A.raw_out && *reinterpret_cast<const unsigned long long*>(A.qd_count + 6) < (unsigned long long)A.dense_rows)
     return;  // batch decision: sparse (the deferred k_query launch finishes the flagged queries)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool str = A.streamed != 0;
+  const bool str = !PAIR && A.streamed != 0;
   const int ng = (qd + A.nq_max - 1) / A.nq_max;               // query groups
-  const int nq = ((qd + ng - 1) / ng + 15) / 16 * 16;          // columns per group (MMA N), <= nq_max
+  const int NQA = PAIR ? 32 : 16;                              // (a pair splits the columns in two halves of 16k)
+  const int nq = ((qd + ng - 1) / ng + NQA - 1) / NQA * NQA;   // columns per group (MMA N), <= nq_max
   const int G = gridDim.x, b = blockIdx.x;
-  const int cpg = G / ng;
-  if (b >= cpg * ng) return;                                   // (only with more groups than CTAs / group)
-  const int grp = b % ng, twin = b / ng;
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const int W = PAIR ? G / 2 : G, wb = PAIR ? b >> 1 : b;      // workers (CTAs or pairs) and this one's index
+  const int cpg = W / ng;
+  if (wb >= cpg * ng) return;                                  // (only with more groups than workers / group)
+  const int grp = wb % ng, twin = wb / ng;
   const int q0 = grp * nq, nqv = qd - q0 < nq ? qd - q0 : nq;  // valid columns of this group
   const int KC = A.KC;
-  const int bres = str ? 0 : KC * nq * 128;                    // resident query bytes (RES)
+  const int nqb = PAIR ? nq / 2 : nq;                          // query rows of the group held by this CTA
+  const int bres = str ? 0 : KC * nqb * 128;                   // resident query bytes (RES)
   const int sbytes = str ? 2 * DA_BYTES + nq * 128 : DA_BYTES; // one ring stage: a K chunk of the unit
   // k > 1: per-CTA UB lists in shared memory if they fit next to a ring of >= 3 stages (else global)
   const int lbytes = A.k > 1 ? (nq * A.k * 4 + nq * 8 + 15) / 16 * 16 : 0;
   const bool local_lists = A.k > 1 && !A.raw_out && A.smem_dyn - 1024 - bres - D_MISC - lbytes >= 3 * sbytes;
   int S = (A.smem_dyn - 1024 - bres - D_MISC - (local_lists ? lbytes : 0)) / sbytes;  // as deep as the rest allows
   S = S > D_MAX_STAGES ? D_MAX_STAGES : S;
-  unsigned char* sB = dsm;                                     // RES: KC x nq x 128 B
+  unsigned char* sB = dsm;                                     // RES: KC x nqb x 128 B
   unsigned char* sA = dsm + bres;                              // S stages
   float* s_d = reinterpret_cast<float*>(sA + (size_t)S * sbytes);  // nq: thr + eps - |q^|^2
   float* s_qn = s_d + 256;                                         // nq: |q^|^2
@@ -311,7 +363,7 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* bfull = tfull + 4;
   const int64_t T = A.n_tiles;
-  const int64_t U = str ? (T + 1) / 2 : T;  // work units
+  const int64_t U = (str || PAIR) ? (T + 1) / 2 : T;  // work units
   const int64_t slice_cap = A.cand_cap / G;
   unsigned long long* slice = A.cand + (int64_t)b * slice_cap;
 
@@ -322,7 +374,7 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4 * 32);  // the 4 warps of epilogue group s
+      mbar_init(&tempty[s], (PAIR ? 2 : 1) * 4 * 32);  // the 4 warps of epilogue group s (of both CTAs)
     }
     mbar_init(bfull, 1);
     s_done = 0;
@@ -348,19 +400,37 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     }
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {  // both CTAs of the pair, same warp
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync_all();  // both CTAs' barriers initialised before any TMA / remote arrive targets them
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
+  // PAIR: the leader CTA's barriers, as cluster addresses (TMA transaction bytes, accumulator releases)
+  const uint32_t lead_full0 = PAIR ? mapa_rank(&full[0], 0) : 0u, lead_bfull = PAIR ? mapa_rank(bfull, 0) : 0u;
+  const uint32_t lead_tempty0 = PAIR ? mapa_rank(&tempty[0], 0) : 0u;
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
-      if (!str) {  // the group's queries: every K chunk, 16 rows per box, resident for the whole pass
+      if (PAIR) {  // this CTA's half of the group's queries; the transaction bytes count at the leader
+        if (rank == 0) mbar_expect_tx(bfull, (uint32_t)(KC * nq * 128));
+        const int qh = q0 + (int)rank * nqb;
+        for (int kc = 0; kc < KC; ++kc)
+          for (int r = 0; r < nqb; r += 16)
+            tma_load_2d_pair(sB + ((size_t)kc * nqb + r) * 128, &tmB, kc * DKC, qh + r, lead_bfull);
+      } else if (!str) {  // the group's queries: every K chunk, 16 rows per box, resident for the whole pass
         mbar_expect_tx(bfull, (uint32_t)(KC * nq * 128));
         for (int kc = 0; kc < KC; ++kc)
           for (int r = 0; r < nq; r += 16) tma_load_2d(sB + ((size_t)kc * nq + r) * 128, &tmB, kc * DKC, q0 + r, bfull);
@@ -371,7 +441,7 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       int64_t j = 0;
       int twin_lo = 0;  // the slowest twin's progress, re-read only when this CTA would run too far ahead
       for (int64_t u = twin; u < U; u += cpg, ++j) {
-        if (ng > 1 && !(A.diag & 4) && twin_lo < j - D_AHEAD) {  // stay within D_AHEAD units of the twins
+        if (!PAIR && ng > 1 && !(A.diag & 4) && twin_lo < j - D_AHEAD) {  // stay within D_AHEAD units of the twins
           for (;;) {                                              // (the tile is still in L2 when they read it)
             int lo = 0x7fffffff;
             for (int o = 0; o < ng; ++o) {
@@ -386,8 +456,14 @@ __global__ void __launch_bounds__(D_THREADS, 1)
         for (int kc = 0; kc < KC; ++kc) {
           mbar_wait(&empty[stage], phase ^ 1);
           unsigned char* st = sA + (size_t)stage * sbytes;
+          if (PAIR) {  // this CTA's 128 rows of the unit's 256; the leader expects both halves
+            if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)(2 * sbytes));
+            tma_load_2d_pair(st, &tmA, kc * DKC, (int)((2 * u + rank) * DM), lead_full0 + 8u * (uint32_t)stage);
+          } else {
           mbar_expect_tx(&full[stage], (uint32_t)sbytes);
-          if (!str) {
+          }
+          if (PAIR) {
+          } else if (!str) {
             tma_load_2d(st, &tmA, kc * DKC, (int)(u * DM), &full[stage]);
           } else {
             tma_load_2d(st, &tmA, kc * DKC, (int)(2 * u * DM), &full[stage]);
@@ -399,14 +475,15 @@ __global__ void __launch_bounds__(D_THREADS, 1)
             phase ^= 1;
           }
         }
-        prog[b] = (int)(j + 1);
+        if (!PAIR) prog[b] = (int)(j + 1);
       }
-      prog[b] = 0x7fffffff;  // done: never holds a twin back
+      if (!PAIR) prog[b] = 0x7fffffff;  // done: never holds a twin back
+      if (PAIR) *(volatile int*)&s_done = 1;  // (the peer CTA issues no MMA: its refresher stops here)
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer (one thread)
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16(nq);
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc = idesc_bf16(nq, PAIR ? 2 * DM : DM);
       if (!str) mbar_wait(bfull, 0);
       tc_fence_after();
       int stage = 0;
@@ -414,7 +491,9 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       int64_t j = 0;
       for (int64_t u = twin; u < U; u += cpg, ++j) {
         const int acc = str ? 0 : (int)(j & 1);
-        if (!str) {
+        if (PAIR) {
+          mbar_wait(&tempty[acc], (uint32_t)((j >> 1) & 1) ^ 1);
+        } else if (!str) {
           mbar_wait(&tempty[acc], (uint32_t)((j >> 1) & 1) ^ 1);
         } else {  // both buffers: the unit's two tiles
           mbar_wait(&tempty[0], (uint32_t)(j & 1) ^ 1);
@@ -425,7 +504,13 @@ __global__ void __launch_bounds__(D_THREADS, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + (size_t)stage * sbytes);
-          if (!str) {
+          if (PAIR) {  // M = 256: A rows from both CTAs, B halves from both CTAs (same shared offsets)
+            const uint32_t b0 = smem_u32(sB + (size_t)kc * nqb * 128);
+            const uint32_t dt = tmem + (uint32_t)(acc * 256);
+#pragma unroll
+            for (int kk = 0; kk < DKC / 16; ++kk)
+              tc_mma_bf16_pair(dt, sdesc_sw128(a0 + 32 * kk), sdesc_sw128(b0 + 32 * kk), idesc, (kc | kk) ? 1u : 0u);
+          } else if (!str) {
             const uint32_t b0 = smem_u32(sB + (size_t)kc * nq * 128);
             const uint32_t dt = tmem + (uint32_t)(acc * 256);
 #pragma unroll
@@ -440,13 +525,18 @@ __global__ void __launch_bounds__(D_THREADS, 1)
                           (kc | kk) ? 1u : 0u);
             }
           }
-          tc_commit(&empty[stage]);
+          if (PAIR)
+            tc_commit_pair(&empty[stage]);
+          else
+            tc_commit(&empty[stage]);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if (!str) {
+        if (PAIR) {
+          tc_commit_pair(&tfull[acc]);
+        } else if (!str) {
           tc_commit(&tfull[acc]);
         } else {
           tc_commit(&tfull[0]);
@@ -481,7 +571,10 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     const float nlen = (float)A.len;
     // the i-th tile of this group
     auto exists = [&](int64_t i) -> bool { return str ? twin + i * cpg < U : twin + (2 * i + grp_e) * cpg < U; };
-    auto tile_of = [&](int64_t i) -> int64_t { return str ? 2 * (twin + i * cpg) + grp_e : twin + (2 * i + grp_e) * cpg; };
+    auto tile_of = [&](int64_t i) -> int64_t {
+      if (PAIR) return 2 * (twin + (2 * i + grp_e) * cpg) + rank;  // this CTA's half of the unit
+      return str ? 2 * (twin + i * cpg) + grp_e : twin + (2 * i + grp_e) * cpg;
+    };
     // the row's 1/sigma, loaded a tile (of this group) ahead; |x^|^2 = n, 0 for a constant row, NaN past N
     auto sig_load = [&](int64_t i) -> float {
       const int64_t tt = tile_of(i), rr = tt * DM + r;
@@ -502,7 +595,10 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       const float xn = xnorm_of(sig);
       if (A.diag & 2) {  // timing diagnostic: release the buffer unread
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        if (PAIR)
+          mbar_arrive_cluster(lead_tempty0 + 8u * (uint32_t)acc);
+        else
+          mbar_arrive(&tempty[acc]);
         continue;
       }
       const uint32_t tbase = tmem + ((uint32_t)(qtr * 32) << 16) + (uint32_t)(acc * 256);
@@ -546,14 +642,21 @@ __global__ void __launch_bounds__(D_THREADS, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if (PAIR)
+        mbar_arrive_cluster(lead_tempty0 + 8u * (uint32_t)acc);  // the leader's MMA waits on both CTAs
+      else
+        mbar_arrive(&tempty[acc]);
     }
   }
   __syncthreads();
   if (threadIdx.x == 0 && A.slice_count) A.slice_count[b] = s_ccount;  // candidates of this CTA (may exceed its slice)
+  if (PAIR) cluster_sync_all();  // neither CTA leaves while the pair's MMAs may still read its shared memory
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
 
@@ -575,6 +678,7 @@ struct DensePost {
   int* tki;           // slot x k (local row)
   int* tkn;
   int* lock;
+  unsigned long long* key1;  // slot: k = 1 best key
   const unsigned long long* cand;
   int64_t cand_cap;
   const int* slice_count;  // per screen CTA
@@ -666,8 +770,10 @@ __global__ void __launch_bounds__(kThreads) k_dense_post(const DensePost P) {
       slot = P.ovf_list[(u - nc) / P.n];
       row = (u - nc) % P.n;
     }
+    // abandon / insertion bound: the exact k-th best so far, and the screen's final threshold (a proven
+    // bound on the true k-th best: no top-k row lies above it)
     float bsf = 0.f;
-    if (lane == 0) bsf = *(volatile float*)&P.bsf[slot];
+    if (lane == 0) bsf = fminf(*(volatile float*)&P.bsf[slot], *(volatile float*)&P.thr[slot]);
     bsf = __shfl_sync(FULL, bsf, 0);
     const float* rows[1] = {P.series + row * P.len};
     const float2 st[1] = {P.stats_orig[row]};
@@ -678,8 +784,14 @@ __global__ void __launch_bounds__(kThreads) k_dense_post(const DensePost P) {
                          ab);
     ++n_ref;
     if (lane == 0 && !ab[0]) {
-      const int n = *(volatile int*)&P.tkn[slot];
-      if (n < P.k || d2[0] <= bsf) g_topk_insert(P, slot, d2[0], (int)row);
+      if (P.k == 1) {  // lock-free: the minimum of (d^2 bits, row) keys is the (distance, index) minimum
+        if (d2[0] <= P.binit[slot]) {
+          atomicMin(&P.key1[slot], ((unsigned long long)__float_as_uint(d2[0]) << 32) | (uint32_t)row);
+          atomicMin(reinterpret_cast<unsigned int*>(&P.bsf[slot]), __float_as_uint(d2[0]));  // abandon bound
+        }
+      } else if (d2[0] <= bsf) {
+        g_topk_insert(P, slot, d2[0], (int)row);
+      }
     }
   }
   if (P.dstats && lane == 0 && n_ref) atomicAdd(&P.dstats[21], (unsigned long long)n_ref);
@@ -693,6 +805,14 @@ __global__ void __launch_bounds__(kThreads) k_dense_post(const DensePost P) {
   __threadfence();
   for (int slot = threadIdx.x; slot < qd; slot += kThreads) {
     const int qi = P.qidx[slot];
+    if (P.k == 1) {
+      const unsigned long long key = *(volatile unsigned long long*)&P.key1[slot];
+      P.tkn[slot] = key != ~0ull;
+      if (key != ~0ull) {
+        P.tkd[slot] = __uint_as_float((uint32_t)(key >> 32));
+        P.tki[slot] = (int)(uint32_t)key;
+      }
+    }
     write_topk(P.tkd + (int64_t)slot * P.k, P.tki + (int64_t)slot * P.k, *(volatile int*)&P.tkn[slot], P.k, P.goff,
                P.od + (int64_t)qi * P.k, P.oi + (int64_t)qi * P.k);
   }
@@ -743,10 +863,11 @@ static int make_tmap_bf16(CUtensorMap* m, const __nv_bfloat16* base, int64_t row
 // launch geometry of the screen for row length `len`: the queries per group that fit next to an A ring
 // of at least 4 stages (multiple of 16, <= 256 for the 2 x 256 TMEM accumulator columns); the kernel
 // then deepens the ring into whatever its group's queries leave free (up to D_MAX_STAGES)
-static void dense_geometry(int len, int& nq_max, int& streamed) {
+static void dense_geometry(int len, bool pair, int& nq_max, int& streamed) {
   const int KC = (len + DKC - 1) / DKC;
   const int avail = D_SMEM_MAX - 1024 - 4 * DA_BYTES - D_MISC;
-  const int nq = avail / (KC * 128) / 16 * 16;
+  const int nq = pair ? avail / (KC * 64) / 32 * 32   // a CTA of a pair holds half of the group's queries
+                      : avail / (KC * 128) / 16 * 16;
   if (nq >= 128) {  // RES: queries resident next to a ring of >= 4 row-tile stages
     nq_max = nq > 256 ? 256 : nq;
     streamed = 0;
@@ -758,24 +879,32 @@ static void dense_geometry(int len, int& nq_max, int& streamed) {
 
 static int launch_screen(sofa_index* ix, const CUtensorMap& tmA, const CUtensorMap& tmB, const DenseArgs& A,
                          size_t smem, cudaStream_t st) {
-  static std::atomic<uint32_t> attr_set{0};  // per device: the smem attribute is set once
+  static std::atomic<uint32_t> attr_set{0};  // per device: the smem attributes are set once
   const uint32_t bit = 1u << (ix->device & 31);
   if (!(attr_set.load() & bit)) {
-    SOFA_CK(cudaFuncSetAttribute(k_dense_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, D_SMEM_MAX));
+    SOFA_CK(cudaFuncSetAttribute(k_dense_screen<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, D_SMEM_MAX));
+    SOFA_CK(cudaFuncSetAttribute(k_dense_screen<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, D_SMEM_MAX));
     attr_set.fetch_or(bit);
   }
-  // cooperative: every CTA resident at once (the twins wait on each other's progress)
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(ix->sms);
+  cfg.gridDim = dim3(ix->sms & ~1);
   cfg.blockDim = dim3(D_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  SOFA_CK(cudaLaunchKernelEx(&cfg, k_dense_screen, tmA, tmB, A));
+  if (A.pair) {  // RES on CTA pairs (clusters of 2 on one TPC); no CTA waits on another pair
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    SOFA_CK(cudaLaunchKernelEx(&cfg, k_dense_screen<true>, tmA, tmB, A));
+  } else {  // STR: cooperative, every CTA resident at once (the twins wait on each other's progress)
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    SOFA_CK(cudaLaunchKernelEx(&cfg, k_dense_screen<false>, tmA, tmB, A));
+  }
   SOFA_LAUNCHED();
   return SOFA_OK;
 }
@@ -788,7 +917,8 @@ static void fill_screen_args(sofa_index* ix, int k, DenseArgs& A) {
   A.k = k;
   A.KC = (ix->len + DKC - 1) / DKC;
   A.n_tiles = (ix->n + DM - 1) / DM;
-  dense_geometry(ix->len, A.nq_max, A.streamed);
+  dense_geometry(ix->len, ix->tune.dense_pair != 0, A.nq_max, A.streamed);
+  A.pair = !A.streamed && ix->tune.dense_pair != 0;
   A.smem_dyn = D_SMEM_MAX;
   A.stats_orig = ix->stats_orig;
   A.qd_count = D.counters;
@@ -842,11 +972,12 @@ int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stat
   P.tkd = D.tkd;
   P.tki = D.tki;
   P.tkn = D.tkn;
+  P.key1 = D.key1;
   P.lock = D.lock;
   P.cand = D.cand;
   P.cand_cap = D.cand_cap;
   P.slice_count = A.slice_count;
-  P.nslices = ix->sms;
+  P.nslices = ix->sms & ~1;  // the screen's grid (an even number of CTAs: pairs)
   P.overflow = D.overflow;
   P.ovf_list = D.ovf_list;
   P.ovf_count = D.counters + 1;
@@ -904,7 +1035,7 @@ int dense_dots(const float* rows, int64_t m, int len, const float* queries, int 
     A.k = 1;
     A.KC = (len + DKC - 1) / DKC;
     A.n_tiles = (m + DM - 1) / DM;
-    dense_geometry(len, A.nq_max, A.streamed);
+    dense_geometry(len, false, A.nq_max, A.streamed);
     A.smem_dyn = D_SMEM_MAX;
     A.progress = prog;
     A.raw_out = out;
@@ -940,6 +1071,7 @@ int ensure_dense_scratch(sofa_index* ix, int q, int k) {
   SOFA_CK(cudaMalloc(&D.tkd, (size_t)q * k * 4));
   SOFA_CK(cudaMalloc(&D.tki, (size_t)q * k * 4));
   SOFA_CK(cudaMalloc(&D.tkn, (size_t)q * 4));
+  SOFA_CK(cudaMalloc(&D.key1, (size_t)q * 8));
   SOFA_CK(cudaMalloc(&D.lock, (size_t)q * 4));
   SOFA_CK(cudaMalloc(&D.ubl, (size_t)q * k * 4));
   SOFA_CK(cudaMalloc(&D.ubn, (size_t)q * 4));
@@ -953,7 +1085,7 @@ int ensure_dense_scratch(sofa_index* ix, int q, int k) {
 
 void free_dense_scratch(sofa_index* ix) {
   DenseScratch& D = ix->dense;
-  void* ps[] = {D.qhat, D.qb16, D.qparams, D.qidx, D.binit, D.bsf, D.thr, D.tkd, D.tki, D.tkn, D.lock, D.ubl,
+  void* ps[] = {D.qhat, D.qb16, D.qparams, D.qidx, D.binit, D.bsf, D.thr, D.tkd, D.tki, D.tkn, D.key1, D.lock, D.ubl,
                 D.ubn, D.ub_lock, D.overflow, D.ovf_list, D.cand, D.counters};
   for (void* p : ps)
     if (p) cudaFree(p);

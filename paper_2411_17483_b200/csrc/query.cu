@@ -124,6 +124,7 @@ struct QArgs {
   int* d_qidx;
   float *d_binit, *d_bsf, *d_thr, *d_tkd;
   int *d_tki, *d_tkn, *d_lock, *d_overflow;
+  unsigned long long* d_key1;
   float weights[SOFA_MAX_L];
 };
 
@@ -1240,6 +1241,7 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
             A.d_bsf[slot] = S.bsf;
             A.d_thr[slot] = S.tkn == A.k ? S.bsf : S.bsf_init;  // proven bound on the k-th best (or +inf)
             A.d_tkn[slot] = S.tkn;
+            A.d_key1[slot] = S.tkn > 0 ? ((unsigned long long)__float_as_uint(s_tkd[0]) << 32) | (uint32_t)s_tki[0] : ~0ull;
             A.d_lock[slot] = 0;
             A.d_ubn[slot] = 0;
             A.d_ublock[slot] = 0;
@@ -1515,6 +1517,7 @@ int launch_query_impl(sofa_index* ix, const float* Q, int q, int k, const float*
     A.d_tkd = D.tkd;
     A.d_tki = D.tki;
     A.d_tkn = D.tkn;
+    A.d_key1 = D.key1;
     A.d_lock = D.lock;
     A.d_overflow = D.overflow;
   }

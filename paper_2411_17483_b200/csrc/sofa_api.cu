@@ -176,6 +176,7 @@ int sofa_default_tuning(sofa_tuning* out) {
   out->dense_cand_cap = 0;
   out->dense_diag = 0;
   out->dense_batch_rows = 0;
+  out->dense_pair = 0;
   return SOFA_OK;
 }
 
@@ -377,10 +378,10 @@ int sofa_build(const float* series_dev, int64_t n, int32_t len, int32_t l, int32
       ix->dense_permille = 0;
     }
   }
-  // (the model phase ends here: it includes the index allocations above, which are host-synchronous)
-  cudaEventRecord(ev.e[1], st);
+  // (the model phase ends where the transform kernel starts: it includes the index allocations above
+  // and the transform's host-side setup, which are host-synchronous)
   if ((rc = launch_transform(series_dev, n, ix->dm, ix->model, words_u, stats_u, keys_u, nullptr, nullptr, ix->xb16,
-                             st))) {
+                             st, ev.e[1]))) {
     freeall();
     return bail(rc);
   }

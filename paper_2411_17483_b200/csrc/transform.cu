@@ -55,6 +55,8 @@ __device__ __forceinline__ void reduce_scatter_g(float* v, int lane) {
   }
 }
 
+constexpr int kEdgeLd = 257;  // shared-memory row stride of the edge table (floats)
+
 struct TransformArgs {
   const float* X;
   int64_t N;
@@ -82,13 +84,15 @@ __global__ void __launch_bounds__(kThreads, (FOLD || LT > 16) ? 2 : 3) k_transfo
   constexpr int OWN = LT >= G ? 1 : G / LT;   // lanes sharing one value when LT < G
   const int len = A.len, nf4 = len >> 2, l = A.l;
   float4* s_basis = reinterpret_cast<float4*>(smem);                           // LT x NS x G
-  float* s_edges = reinterpret_cast<float*>(smem + (size_t)LT * NS * G * 16);  // LT x 256 (model order)
-  uint8_t* s_w = reinterpret_cast<uint8_t*>(s_edges + LT * 256);               // 8 warps x RPW x LT
+  // LT x kEdgeLd (model order): rows padded to 257 floats so that the lanes of a warp, each searching
+  // its own position's row, start in different banks (a 256-float stride put every row in one bank)
+  float* s_edges = reinterpret_cast<float*>(smem + (size_t)LT * NS * G * 16);
+  uint8_t* s_w = reinterpret_cast<uint8_t*>(s_edges + LT * kEdgeLd);          // 8 warps x RPW x LT
   int* s_ord = reinterpret_cast<int*>(s_w + 8 * RPW * LT);                      // LT
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane & (G - 1), rw = lane / G;  // lane in group, row of the warp
   for (int i = tid; i < LT * NS * G; i += kThreads) s_basis[i] = reinterpret_cast<const float4*>(A.basis)[i];
-  for (int i = tid; i < LT * 256; i += kThreads) s_edges[i] = A.edges32[i];
+  for (int i = tid; i < LT * 256; i += kThreads) s_edges[(i >> 8) * kEdgeLd + (i & 255)] = A.edges32[i];
   for (int i = tid; i < 8 * RPW * LT; i += kThreads) s_w[i] = 0;
   for (int i = tid; i < LT; i += kThreads) s_ord[i] = A.order[i];
   __syncthreads();
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, (FOLD || LT > 16) ? 2 : 3) k_transfo
           const double vd = (double)a * inv64;
           if (A.vals && live) A.vals[row * l + j] = vd;
           const float v = (float)vd;
-          const float* e = s_edges + j * 256;
+          const float* e = s_edges + j * kEdgeLd;
           int pos = 0;
 #pragma unroll
           for (int step = 128; step >= 1; step >>= 1)
@@ -307,7 +311,8 @@ int transform_layout(const DevModel& dm, const sofa_model& m, int G, bool fold, 
 }
 
 template <int G, int LT, bool FOLD>
-static int launch_transform_t(const TransformArgs& A0, const DevModel& dm, const sofa_model& m, cudaStream_t st) {
+static int launch_transform_t(const TransformArgs& A0, const DevModel& dm, const sofa_model& m, cudaStream_t st,
+                              cudaEvent_t t_start) {
   TransformArgs A = A0;
   std::vector<float> hb;
   std::vector<int> ord;
@@ -325,7 +330,7 @@ static int launch_transform_t(const TransformArgs& A0, const DevModel& dm, const
   A.n_re_odd = no;
   constexpr int RPW = 32 / G, NS = FOLD ? 4 : 8;
   auto kern = k_transform<G, LT, FOLD>;
-  const size_t smem = (size_t)LT * NS * G * 16 + (size_t)LT * 256 * 4 + 8 * RPW * LT + LT * 4;
+  const size_t smem = (size_t)LT * NS * G * 16 + (size_t)LT * kEdgeLd * 4 + 8 * RPW * LT + LT * 4;
   SOFA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
@@ -335,6 +340,7 @@ static int launch_transform_t(const TransformArgs& A0, const DevModel& dm, const
   const int64_t want = (A.N + 8 * RPW - 1) / (8 * RPW);
   int grid = (int)(want < (int64_t)sms * per_sm ? want : (int64_t)sms * per_sm);
   if (grid < 1) grid = 1;
+  if (t_start) cudaEventRecord(t_start, st);  // the kernel alone (after the host-side setup above)
   kern<<<grid, kThreads, smem, st>>>(A);
   SOFA_LAUNCHED();
   cudaFreeAsync(db, st);
@@ -344,7 +350,7 @@ static int launch_transform_t(const TransformArgs& A0, const DevModel& dm, const
 
 int launch_transform(const float* X, int64_t N, const DevModel& dm, const sofa_model& m, uint8_t* words,
                      float2* stats, uint64_t* keys, double* vals, uint8_t* words_l, __nv_bfloat16* xb16,
-                     cudaStream_t st) {
+                     cudaStream_t st, cudaEvent_t t_start) {
   if (N <= 0) return SOFA_OK;
   const int nf4 = dm.len / 4;
   int G = 1;
@@ -368,7 +374,8 @@ int launch_transform(const float* X, int64_t N, const DevModel& dm, const sofa_m
   A.xb_ld = (dm.len + 7) / 8 * 8;
 #define SOFA_TR(g, lt)                                                                        \
   if (G == g && dm.LT == lt)                                                                  \
-    return fold ? launch_transform_t<g, lt, true>(A, dm, m, st) : launch_transform_t<g, lt, false>(A, dm, m, st);
+    return fold ? launch_transform_t<g, lt, true>(A, dm, m, st, t_start)                  \
+                : launch_transform_t<g, lt, false>(A, dm, m, st, t_start);
   SOFA_TR(1, 16) SOFA_TR(2, 16) SOFA_TR(4, 16) SOFA_TR(8, 16) SOFA_TR(16, 16) SOFA_TR(32, 16)
   SOFA_TR(1, 32) SOFA_TR(2, 32) SOFA_TR(4, 32) SOFA_TR(8, 32) SOFA_TR(16, 32) SOFA_TR(32, 32)
   SOFA_TR(1, 64) SOFA_TR(2, 64) SOFA_TR(4, 64) SOFA_TR(8, 64) SOFA_TR(16, 64) SOFA_TR(32, 64)

@@ -168,3 +168,17 @@ def test_dense_dots_within_bound(n, q, m):
     bound = gamma * np.linalg.norm(x.astype(np.float64), axis=1)[:, None] * np.linalg.norm(qs.astype(np.float64), axis=1)[None, :]
     assert np.all(tot <= bound + 1e-30), (tot / np.maximum(bound, 1e-30)).max()
     assert np.all(hw[80:90] == 0.0)
+
+
+@pytest.mark.parametrize("kind,N,k,Q", [("cfg3", 30_000 + 5, 1, 300), ("cfg3", 20_000, 6, 70), ("cfg4", 60_000, 1, 90)])
+def test_dense_pair_mode_identical(kind, N, k, Q):
+    """the screen on CTA pairs (tcgen05 cta_group::2, M = 256, each CTA holding half of a query group)
+    returns the same bits as the single-CTA screen, and both match the oracle"""
+    w = datagen.scaled(datagen.WORKLOADS[kind], N, Q)
+    x, q = _data(w)
+    ix, d1, i1, st = _check(x, q, k, sample_size=datagen.default_sample_size(w), dense_permille=1000)
+    assert st["dense_queries"] == Q
+    ix.set_tuning(dense_pair=1)
+    d2, i2, st2 = ix.knn(q, k, stats=True)
+    assert st2["dense_queries"] == Q
+    assert torch.equal(i1, i2) and torch.equal(d1, d2)
