@@ -23,8 +23,8 @@ ix = SofaIndex(x, l=w.l, alphabet=w.alphabet, sample_size=datagen.default_sample
 _, _, st = ix.knn(q, w.k, stats=True)
 print(f"{cfg} N={w.n_series} dense queries {st['dense_queries']} candidates {st['dense_candidates']}", flush=True)
 flops = 2.0 * st["dense_queries"] * w.n_series * w.length
-for diag in (0, 1, 2, 4, 8, 0):
-    ix.set_tuning(dense_diag=diag)
+for pair, diag in ((0, 0), (0, 1), (0, 2), (0, 4), (0, 8), (1, 0), (1, 1), (1, 2), (0, 0)):
+    ix.set_tuning(dense_diag=diag, dense_pair=pair)
     for _ in range(2):
         ix.knn(q, w.k)
     torch.cuda.synchronize()
@@ -33,6 +33,6 @@ for diag in (0, 1, 2, 4, 8, 0):
         ix.knn(q, w.k)
     km, groups = ix.kernel_timing(0)
     dense = km["dense"] / 5
-    print(f"diag {diag}: front {km['front'] / 5:.3f} ms  dense {dense:.3f} ms ({flops / dense / 1e9:.0f} TFLOP/s)"
+    print(f"pair {pair} diag {diag}: front {km['front'] / 5:.3f} ms  dense {dense:.3f} ms ({flops / dense / 1e9:.0f} TFLOP/s)"
           f"  scan {km['scan'] / 5:.3f} ms", flush=True)
-ix.set_tuning(dense_diag=0)
+ix.set_tuning(dense_diag=0, dense_pair=0)
