@@ -153,6 +153,10 @@ typedef struct {
                               screen skip work so its pipeline stages can be timed apart (results are
                               then WRONG): 1 = no screening math, 2 = no TMEM loads either,
                               4 = producers ignore their twins' progress, 8 = no candidate path */
+  int32_t dense_mcast;     /* single-CTA dense screen launched as clusters of 2 (default 1): with an even
+                              number of query groups the two CTAs of a cluster serve two groups over the
+                              same row tiles and share each tile by TMA multicast (one L2 read per tile
+                              for both); 0 = one CTA per worker (cooperative launch) */
 } sofa_tuning;
 
 int sofa_default_tuning(sofa_tuning* out);

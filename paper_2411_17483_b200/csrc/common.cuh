@@ -323,6 +323,7 @@ struct sofa_index {
   int64_t h_cap = 0;
   int device = 0;
   int sms = 148;        // multiprocessors of `device` (queried once at build time)
+  int dense_clusters = 0;  // resident clusters of 2 of the dense screen (queried at its first cluster launch)
   sofa_tuning tune{};   // query-kernel tuning (sofa_set_tuning; defaults from sofa_default_tuning)
   sofa::DevModel dm{};
 };

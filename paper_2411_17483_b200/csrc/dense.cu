@@ -82,6 +82,23 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+// multicast: the box lands at the same shared offset in every CTA of `mask` and completes the transaction
+// bytes on the barrier at the same offset in each of them
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+// arrive (once the prior MMAs complete) on the barrier at this offset in every CTA of `mask`
+__device__ __forceinline__ void tc_commit_mc(uint64_t* b, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(b)),
+               "h"(mask)
+               : "memory");
+}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint64_t* b) {
@@ -185,6 +202,8 @@ struct DenseArgs {
   int raw_ld;
   int raw_q;      // debug: number of query slots (instead of *qd_count)
   int diag;       // sofa_tuning.dense_diag (timing diagnostics; 0 in real use)
+  int cluster2;   // single-CTA screen launched as clusters of 2: an even number of query groups shares
+                  // every row tile by TMA multicast (one L2 read feeds both CTAs of the cluster)
 };
 
 // shared-memory float minimum (values of either sign), rare path
@@ -334,8 +353,15 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
   const int W = PAIR ? G / 2 : G, wb = PAIR ? b >> 1 : b;      // workers (CTAs or pairs) and this one's index
   const int cpg = W / ng;
-  if (wb >= cpg * ng) return;                                  // (only with more groups than workers / group)
-  const int grp = wb % ng, twin = wb / ng;
+  // (idle workers exist only with more groups than workers / group; in a cluster launch they stay for the
+  // cluster barriers, with no work: twin past every unit)
+  const bool idle = wb >= cpg * ng;
+  if (idle && !A.cluster2) return;
+  const int grp = idle ? 0 : wb % ng, twin = idle ? 0x3fffffff : wb / ng;
+  // multicast (clusters of 2, an even number of groups): the cluster's CTAs serve groups 2i, 2i + 1 of the
+  // same twin index, i.e. the same row tiles; each issues half of every tile's K chunks to both
+  const bool mc = !PAIR && A.cluster2 && !A.raw_out && (ng % 2) == 0;
+  const uint32_t crank = (!PAIR && A.cluster2) ? cluster_rank() : 0u;
   const int q0 = grp * nq, nqv = qd - q0 < nq ? qd - q0 : nq;  // valid columns of this group
   const int KC = A.KC;
   const int nqb = PAIR ? nq / 2 : nq;                          // query rows of the group held by this CTA
@@ -370,11 +396,11 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], mc ? 2 : 1);  // multicast: both CTAs' MMAs release the slot
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], (PAIR ? 2 : 1) * 4 * 32);  // the 4 warps of epilogue group s (of both CTAs)
+      mbar_init(&tempty[s], (PAIR ? 2 : 1) * 4);  // one arrive per warp of epilogue group s (of both CTAs)
     }
     mbar_init(bfull, 1);
     s_done = 0;
@@ -411,7 +437,7 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     }
   }
   tc_fence_before();
-  if (PAIR)
+  if (PAIR || A.cluster2)
     cluster_sync_all();  // both CTAs' barriers initialised before any TMA / remote arrive targets them
   else
     __syncthreads();
@@ -440,9 +466,13 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       uint32_t phase = 0;
       int64_t j = 0;
       int twin_lo = 0;  // the slowest twin's progress, re-read only when this CTA would run too far ahead
+      // (a multicast cluster of 2 groups has no twins outside it).  The wait is bounded: a twin that does
+      // not progress for ~1 ms (not resident: another kernel holds its SM) is given up on — only L2 reuse
+      // depends on it, never a result, so no CTA can wait forever on another
+      bool twin_sync = !PAIR && ng > (mc ? 2 : 1) && !(A.diag & 4);
       for (int64_t u = twin; u < U; u += cpg, ++j) {
-        if (!PAIR && ng > 1 && !(A.diag & 4) && twin_lo < j - D_AHEAD) {  // stay within D_AHEAD units of the twins
-          for (;;) {                                              // (the tile is still in L2 when they read it)
+        if (twin_sync && twin_lo < j - D_AHEAD) {  // stay within D_AHEAD units of the twins
+          for (int spin = 0;; ++spin) {            // (the tile is still in L2 when they read it)
             int lo = 0x7fffffff;
             for (int o = 0; o < ng; ++o) {
               const int p = prog[twin * ng + o];
@@ -450,6 +480,10 @@ __global__ void __launch_bounds__(D_THREADS, 1)
             }
             twin_lo = lo;
             if (lo >= j - D_AHEAD) break;
+            if (spin >= 4096) {
+              twin_sync = false;
+              break;
+            }
             __nanosleep(256);
           }
         }
@@ -463,6 +497,8 @@ __global__ void __launch_bounds__(D_THREADS, 1)
           mbar_expect_tx(&full[stage], (uint32_t)sbytes);
           }
           if (PAIR) {
+          } else if (mc) {
+            if ((uint32_t)(kc & 1) == crank) tma_load_2d_mc(st, &tmA, kc * DKC, (int)(u * DM), &full[stage], 3);
           } else if (!str) {
             tma_load_2d(st, &tmA, kc * DKC, (int)(u * DM), &full[stage]);
           } else {
@@ -527,6 +563,8 @@ __global__ void __launch_bounds__(D_THREADS, 1)
           }
           if (PAIR)
             tc_commit_pair(&empty[stage]);
+          else if (mc)
+            tc_commit_mc(&empty[stage], 3);  // the slot is free once BOTH CTAs' MMAs have read it
           else
             tc_commit(&empty[stage]);
           if (++stage == S) {
@@ -584,21 +622,29 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     };
     auto xnorm_of = [&](float sig) -> float { return isnan(sig) ? sig : (sig > 0.f ? nlen : 0.f); };
     const int acc = grp_e;
-    float sig_next = sig_load(0);
+    // the rows' 1/sigma, loaded 4 group tiles ahead: one load per row per tile, but queued behind the TMA
+    // stream it took longer than a tile (ncu: 44% of the kernel's stall samples on its use with 1 ahead)
+    float sig_q0 = sig_load(0), sig_q1 = sig_load(1), sig_q2 = sig_load(2), sig_q3 = sig_load(3);
     for (int64_t i = 0; exists(i); ++i) {
       const uint32_t aph = (uint32_t)(i & 1);
       const int64_t row = tile_of(i) * DM + r;
-      const float sig = sig_next;  // loaded one group tile ahead
-      sig_next = sig_load(i + 1);
+      const float sig = sig_q0;
+      sig_q0 = sig_q1;
+      sig_q1 = sig_q2;
+      sig_q2 = sig_q3;
+      sig_q3 = sig_load(i + 4);
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const float xn = xnorm_of(sig);
       if (A.diag & 2) {  // timing diagnostic: release the buffer unread
         tc_fence_before();
-        if (PAIR)
-          mbar_arrive_cluster(lead_tempty0 + 8u * (uint32_t)acc);
-        else
-          mbar_arrive(&tempty[acc]);
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR)
+            mbar_arrive_cluster(lead_tempty0 + 8u * (uint32_t)acc);
+          else
+            mbar_arrive(&tempty[acc]);
+        }
         continue;
       }
       const uint32_t tbase = tmem + ((uint32_t)(qtr * 32) << 16) + (uint32_t)(acc * 256);
@@ -641,16 +687,21 @@ __global__ void __launch_bounds__(D_THREADS, 1)
         screen(vb, (ch + 1) * 32);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       }
+      // the warp's TMEM reads are complete (tcgen05.wait::ld is warp-wide): one arrive per warp, a remote
+      // one (DSMEM) for the peer CTA of a pair — the leader's MMA waits on both CTAs
       tc_fence_before();
-      if (PAIR)
-        mbar_arrive_cluster(lead_tempty0 + 8u * (uint32_t)acc);  // the leader's MMA waits on both CTAs
-      else
-        mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR)
+          mbar_arrive_cluster(lead_tempty0 + 8u * (uint32_t)acc);
+        else
+          mbar_arrive(&tempty[acc]);
+      }
     }
   }
   __syncthreads();
   if (threadIdx.x == 0 && A.slice_count) A.slice_count[b] = s_ccount;  // candidates of this CTA (may exceed its slice)
-  if (PAIR) cluster_sync_all();  // neither CTA leaves while the pair's MMAs may still read its shared memory
+  if (PAIR || A.cluster2) cluster_sync_all();  // neither CTA leaves while its peer may still read / multicast into its shared memory
   if (warp == 1) {
     tc_fence_after();
     if (PAIR)
@@ -878,7 +929,7 @@ static void dense_geometry(int len, bool pair, int& nq_max, int& streamed) {
 }
 
 static int launch_screen(sofa_index* ix, const CUtensorMap& tmA, const CUtensorMap& tmB, const DenseArgs& A,
-                         size_t smem, cudaStream_t st) {
+                         size_t smem, cudaStream_t st, int* grid_out = nullptr) {
   static std::atomic<uint32_t> attr_set{0};  // per device: the smem attributes are set once
   const uint32_t bit = 1u << (ix->device & 31);
   if (!(attr_set.load() & bit)) {
@@ -899,10 +950,30 @@ static int launch_screen(sofa_index* ix, const CUtensorMap& tmA, const CUtensorM
     at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    if (grid_out) *grid_out = (int)cfg.gridDim.x;
     SOFA_CK(cudaLaunchKernelEx(&cfg, k_dense_screen<true>, tmA, tmB, A));
-  } else {  // STR: cooperative, every CTA resident at once (the twins wait on each other's progress)
+  } else if (A.cluster2) {  // clusters of 2 (TMA multicast when the groups pair up); as many clusters as
+    // can be resident at once (an SM left over in a GPC stays idle rather than running a second wave)
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    if (ix->dense_clusters <= 0) {
+      int nc = 0;
+      cfg.gridDim = dim3(ix->sms & ~1);
+      if (cudaOccupancyMaxActiveClusters(&nc, k_dense_screen<false>, &cfg) != cudaSuccess || nc < 1) {
+        cudaGetLastError();
+        nc = ix->sms / 2;
+      }
+      ix->dense_clusters = nc < ix->sms / 2 ? nc : ix->sms / 2;
+    }
+    cfg.gridDim = dim3(2 * ix->dense_clusters);
+    if (grid_out) *grid_out = (int)cfg.gridDim.x;
+    SOFA_CK(cudaLaunchKernelEx(&cfg, k_dense_screen<false>, tmA, tmB, A));
+  } else {  // cooperative, every CTA resident at once (the twins wait on each other's progress)
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
+    if (grid_out) *grid_out = (int)cfg.gridDim.x;
     SOFA_CK(cudaLaunchKernelEx(&cfg, k_dense_screen<false>, tmA, tmB, A));
   }
   SOFA_LAUNCHED();
@@ -919,6 +990,7 @@ static void fill_screen_args(sofa_index* ix, int k, DenseArgs& A) {
   A.n_tiles = (ix->n + DM - 1) / DM;
   dense_geometry(ix->len, ix->tune.dense_pair != 0, A.nq_max, A.streamed);
   A.pair = !A.streamed && ix->tune.dense_pair != 0;
+  A.cluster2 = !A.pair && ix->tune.dense_mcast != 0;
   A.smem_dyn = D_SMEM_MAX;
   A.stats_orig = ix->stats_orig;
   A.qd_count = D.counters;
@@ -949,9 +1021,10 @@ int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stat
   }
   DenseArgs A{};
   fill_screen_args(ix, k, A);
+  int sgrid = ix->sms & ~1;
   if ((rc = launch_screen(ix, *reinterpret_cast<const CUtensorMap*>(D.tmap_x),
                           *reinterpret_cast<const CUtensorMap*>(D.tmap_q), A, D_SMEM_MAX,
-                          st)))
+                          st, &sgrid)))
     return rc;
   if (after_screen) cudaEventRecord(after_screen, st);
 
@@ -977,7 +1050,7 @@ int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stat
   P.cand = D.cand;
   P.cand_cap = D.cand_cap;
   P.slice_count = A.slice_count;
-  P.nslices = ix->sms & ~1;  // the screen's grid (an even number of CTAs: pairs)
+  P.nslices = sgrid;  // the screen's grid (its CTAs' candidate slices)
   P.overflow = D.overflow;
   P.ovf_list = D.ovf_list;
   P.ovf_count = D.counters + 1;

@@ -177,6 +177,7 @@ int sofa_default_tuning(sofa_tuning* out) {
   out->dense_diag = 0;
   out->dense_batch_rows = 0;
   out->dense_pair = 0;
+  out->dense_mcast = 1;
   return SOFA_OK;
 }
 

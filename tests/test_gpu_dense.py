@@ -182,3 +182,19 @@ def test_dense_pair_mode_identical(kind, N, k, Q):
     d2, i2, st2 = ix.knn(q, k, stats=True)
     assert st2["dense_queries"] == Q
     assert torch.equal(i1, i2) and torch.equal(d1, d2)
+
+
+@pytest.mark.parametrize("kind,N,k,Q", [("cfg3", 30_000 + 5, 1, 300), ("cfg3", 20_000, 4, 600),
+                                        ("cfg3", 12_000, 2, 1000), ("cfg3", 9_000, 1, 100)])
+def test_dense_mcast_identical(kind, N, k, Q):
+    """clusters of 2 sharing row tiles by TMA multicast (an even number of query groups: 300 -> 2,
+    1000 -> 4), or not (600 -> 3 groups, 100 -> 1: clusters without multicast, the idle CTA kept for the
+    cluster barriers) return the same bits as the cooperative one-CTA-per-worker launch"""
+    w = datagen.scaled(datagen.WORKLOADS[kind], N, Q)
+    x, q = _data(w)
+    ix, d1, i1, st = _check(x, q, k, sample_size=datagen.default_sample_size(w), dense_permille=1000)
+    assert st["dense_queries"] == Q
+    ix.set_tuning(dense_mcast=0)
+    d2, i2, st2 = ix.knn(q, k, stats=True)
+    assert st2["dense_queries"] == Q
+    assert torch.equal(i1, i2) and torch.equal(d1, d2)
