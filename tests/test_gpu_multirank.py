@@ -23,7 +23,7 @@ from paper_2411_17483_b200.distributed import ShardedSofa
 from paper_2411_17483_b200.index import SofaIndex
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 torch.cuda.set_device(0)
-dist.init_process_group("gloo")
+dist.init_process_group(os.environ.get("BACKEND", "gloo"))
 w = datagen.scaled(datagen.WORKLOADS[os.environ["CFG"]], int(os.environ["N"]), 64, k=int(os.environ["K"]))
 a, b = datagen.shard_range(w.n_series, rank, world)
 shard = datagen.generate_rows(w, a, b, device="cuda")
@@ -55,6 +55,21 @@ def test_two_ranks_on_one_gpu_equal_single_index(cfg, N, k, tmp_path):
     script.write_text(WORKER)
     env = dict(os.environ, ROOT=ROOT, CFG=cfg, N=str(N), K=str(k))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", str(script)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "MERGED_EQUALS_SINGLE True" in r.stdout, r.stdout[-2000:]
+
+
+@pytest.mark.parametrize("cfg,N,k", [("cfg1", 40_000, 1), ("cfg3", 30_000, 3)])
+def test_nccl_path_on_one_rank(cfg, N, k, tmp_path):
+    """the sharded pipeline over NCCL itself (one rank: this pool has one GPU per box): the model
+    broadcast, the seed-bound all-reduce MIN, and the k = 1 packed-key all-reduce MIN / k > 1
+    all-gather + min-merge run as real NCCL collectives on cuda:0; the answer equals a single index"""
+    script = tmp_path / "worker.py"
+    script.write_text(WORKER)
+    env = dict(os.environ, ROOT=ROOT, CFG=cfg, N=str(N), K=str(k), BACKEND="nccl")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", str(script)]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]

@@ -4,7 +4,7 @@
   * leaf size (Fig. 11): block size B vs query throughput and pruning.
 The paper's datasets are not available; BASELINE.json's configs[1] (10M random walks, 1000
 noisy-member queries) and configs[2] (10M high-frequency, 1000 random queries) stand in.
-python tools/build_sweeps.py [N] > profiles/r01_build_sweeps.md"""
+python tools/build_sweeps.py [N] > profiles/r02_build_sweeps.md"""
 import json
 import os
 import statistics
