@@ -23,8 +23,11 @@ ix = SofaIndex(x, l=w.l, alphabet=w.alphabet, sample_size=datagen.default_sample
 _, _, st = ix.knn(q, w.k, stats=True)
 print(f"{cfg} N={w.n_series} dense queries {st['dense_queries']} candidates {st['dense_candidates']}", flush=True)
 flops = 2.0 * st["dense_queries"] * w.n_series * w.length
-for mc, pair, diag in ((1, 0, 0), (1, 0, 1), (1, 0, 2), (1, 0, 8), (0, 0, 0), (0, 0, 2), (0, 0, 4), (0, 1, 0),
-                      (0, 1, 2), (1, 0, 0)):
+MODES = [(1, 0, 0), (1, 0, 1), (1, 0, 2), (1, 0, 8), (1, 0, 16), (1, 0, 32), (1, 0, 48), (0, 0, 0), (0, 0, 2),
+         (0, 0, 4), (0, 1, 0), (0, 1, 2), (1, 0, 0)]
+if os.environ.get("DIAG_MODES"):
+    MODES = [tuple(int(v) for v in m.split(",")) for m in os.environ["DIAG_MODES"].split(";")]
+for mc, pair, diag in MODES:
     ix.set_tuning(dense_diag=diag, dense_pair=pair, dense_mcast=mc)
     for _ in range(2):
         ix.knn(q, w.k)
