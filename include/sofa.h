@@ -129,7 +129,7 @@ typedef struct {
  * tests check bit-identical outputs across settings).  sofa_default_tuning gives the defaults. */
 typedef struct {
   int32_t front_batches;   /* word batches of LB-ordered leaves the front scans per query before the
-                              rest becomes scan tasks (default 16; >= 1) */
+                              rest becomes scan tasks (0 = 16) */
   int32_t rev_rounds;      /* refine rounds of a leaf part before it is deferred to the revisit pass
                               (default 2; 0 defers every part with a candidate) */
   int32_t topm_min;        /* top-M seeding for leaf lists longer than this (0 => nb/16 clamped to
@@ -157,6 +157,8 @@ typedef struct {
                               number of query groups the two CTAs of a cluster serve two groups over the
                               same row tiles and share each tile by TMA multicast (one L2 read per tile
                               for both); 0 = one CTA per worker (cooperative launch) */
+  int32_t scan_fused;      /* front CTAs that find no query left scan the tasks other fronts publish, in the
+                              same launch (default 1); 0 = only the separate scan launch scans them */
 } sofa_tuning;
 
 int sofa_default_tuning(sofa_tuning* out);

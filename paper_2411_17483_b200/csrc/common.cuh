@@ -303,6 +303,9 @@ struct sofa_index {
   // front/scan split (query.cu): per-query state, tables, the leaf pool and the scan tasks
   void *qstate = nullptr, *q_T = nullptr, *q_hat = nullptr, *pool = nullptr, *tasks = nullptr,
        *rank_count = nullptr;
+  void *fifo = nullptr, *fifo_seq = nullptr;  // fused scan: published set-0 tasks in publication order
+  int* fcount = nullptr;  // fused-scan counters (512 B: one 128-byte line each)
+  int epoch = 0;  // front launch number: FIFO entries and query states are valid when they carry it
   int64_t scan_q_cap = 0, pool_cap = 0, task_cap = 0, rank_cap = 0;
   int scan_LT = 0;
   unsigned long long* dstats = nullptr;

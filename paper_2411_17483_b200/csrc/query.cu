@@ -54,6 +54,7 @@ constexpr int kFan = 16;  // envelope tree fan-out
 // output.  Results do not depend on which CTA scans which chunk.
 struct QState {
   int tkn, lock, ntasks, done;
+  int ready;  // == the front launch's epoch once the front has handed the query over (tables, top-k, ntasks)
   float bsf, bsf_init;
   float tkd[SOFA_MAX_K];
   int tki[SOFA_MAX_K];
@@ -115,6 +116,13 @@ struct QArgs {
   int* rank_count;     // 2 x rank_cap
   int rank_cap;
   int* counters;       // [2s] ranks used in set s, [2s+1] its cursor
+  int* fcount;         // fused scan, one 128-byte line each: [0] fronts finished, [32] FIFO entries
+                       // reserved, [64] FIFO tickets taken
+  ScanTask* fifo;      // fused scan: set-0 tasks in publication order (instead of the rank-major table)
+  int* fifo_seq;       // == epoch once fifo[i] is written (fifo_cap entries)
+  int64_t fifo_cap;
+  int epoch;
+  int fused;           // front CTAs without a query left scan the set-0 tasks other fronts publish
   int* qd_counter;
   float* d_qhat;
   __nv_bfloat16* d_qb16;
@@ -176,6 +184,7 @@ struct QShared {
   // per query: 0 blocks_survived, 1 words_scanned, 2 candidates, 3 refined, 4 abandoned, 5 env_nodes,
   // 6 list_blocks, 7 rounds, 8 batches, 9 waves
   unsigned int st[10];
+  int fpos[2], fcnt[2], nf;  // fused scan: this query's FIFO ranges, made visible at its handoff
 };
 
 // word LB (d_SFA^2 from the T table) with chunked early abandoning: Alg. 3.  The word's
@@ -332,7 +341,8 @@ __device__ void scan_blocks(const QArgs& A, QShared& S, const unsigned long long
       const int e = u / ppl, part = u % ppl;
       unsigned long long ent;
       if (list) {
-        ent = list[e];
+        // a pool list may have been written by another SM in this launch (fused scan): read it from L2
+        ent = __isGlobal(list + e) ? __ldcg(list + e) : list[e];
       } else {  // range task: the leaf's envelope LB, lane j < LT takes position j
         const int64_t leaf = range0 + e;
         const uint8_t* ev = A.env + leaf * 2 * A.WS;
@@ -504,7 +514,7 @@ __device__ void publish_tasks(const QArgs& A, QShared& S, int q, const unsigned 
     S.off = (long long)atomicAdd(A.pool_used, (unsigned long long)n);
     S.chunk = S.ntask;
     S.ntask += (n + CH - 1) / CH;
-    atomicMax(&A.counters[2 * set], S.ntask);
+    if (!(A.fused && set == 0)) atomicMax(&A.counters[2 * set], S.ntask);
   }
   __syncthreads();
   const int CH = S.chsz;
@@ -513,6 +523,27 @@ __device__ void publish_tasks(const QArgs& A, QShared& S, int q, const unsigned 
   const int r0 = S.chunk;
   for (int i = tid; i < n; i += kQThreads) A.pool[off + i] = list[i];
   const int flags = sorted ? kTaskSorted : 0;
+  if (A.fused && set == 0) {
+    // fused scan: a contiguous FIFO range for this call's tasks; their sequence numbers are written at
+    // the query's handoff (after its state), so a consumer never holds a task it cannot start yet
+    if (tid == 0) {
+      S.fpos[S.nf] = atomicAdd(A.fcount + 32, nt);
+      S.fcnt[S.nf] = nt;
+      S.nf++;
+    }
+    __syncthreads();
+    const int p0 = S.fpos[S.nf - 1];
+    for (int i = tid; i < nt; i += kQThreads) {
+      ScanTask t;
+      t.off = off + (int64_t)i * CH;
+      t.q = q;
+      t.cnt_flags = (n - i * CH < CH ? n - i * CH : CH) | flags;
+      A.fifo[p0 + i] = t;
+    }
+    __threadfence();  // this thread's pool entries and records, before the handoff's sequence numbers
+    __syncthreads();
+    return;
+  }
   ScanTask* tasks = A.tasks + (int64_t)set * A.rank_cap * A.q;
   int* rc = A.rank_count + set * A.rank_cap;
   for (int i = tid; i < nt; i += kQThreads) {
@@ -564,7 +595,7 @@ __device__ void publish_range(const QArgs& A, QShared& S, int q) {
 // LB chunk first), so a query's later chunks usually meet its final BSF and are rejected unread
 template <int LT, int NF, int RR = refine_rows<NF>()>
 __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd, int* s_tki, float4* s_qh4,
-                           float* s_env) {
+                           float* s_env, bool fused = false) {
   const int tid = threadIdx.x;
   bool dense_go = false;
   if (A.qd_counter) {
@@ -581,7 +612,38 @@ __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd,
   }
   int cur = -1, cur_env = -1;
   for (;;) {
-    if (tid == 0) {
+    if (fused && tid == 0) {
+      // a ticket = the next FIFO entry in publication order; wait until it is published, or until every
+      // front has finished and the FIFO ends before it (then this CTA is done).  Every cross-CTA read
+      // below is volatile or ld.global.cg (no L1-invalidating fence on the consumer side).
+      // The counters live on separate 128-byte lines and a waiting CTA backs off exponentially (64 ns
+      // .. 4 us): hundreds of idle CTAs polling one L2 line at full rate slowed the fronts still running.
+      int have = 0;
+      const int t = atomicAdd(A.fcount + 64, 1);
+      unsigned ns = 64;
+      for (;;) {
+        if (t < A.fifo_cap && *(volatile int*)&A.fifo_seq[t] == A.epoch) {
+          have = 1;
+          break;
+        }
+        if (*(volatile int*)A.fcount >= A.q && *(volatile int*)(A.fcount + 32) <= t) break;
+        __nanosleep(ns);
+        ns = ns < 4096 ? 2 * ns : 4096;
+      }
+      s_have = have;
+      if (have) {
+        const volatile ScanTask* vt = &A.fifo[t];
+        ScanTask tk;
+        tk.off = vt->off;
+        tk.q = vt->q;
+        tk.cnt_flags = vt->cnt_flags;
+        s_task = tk;
+        volatile QState* h = &A.qs[tk.q];
+        while (h->ready != A.epoch) __nanosleep(64);  // its front is still publishing
+        const float thr = thr_of(h->bsf);
+        S.take = (tk.cnt_flags & kTaskSorted) && lb_of(__ldcg(A.pool + tk.off)) > thr;
+      }
+    } else if (tid == 0) {
       int have = 0;
       for (int set = 0; set < nsets && !have; ++set) {
         const int ranks = A.counters[2 * set] < A.rank_cap ? A.counters[2 * set] : A.rank_cap;
@@ -614,8 +676,9 @@ __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd,
     if (!S.take) {
       if (q != cur) {
         const float4* T4 = reinterpret_cast<const float4*>(A.q_T + (int64_t)q * 3 * LT * 256);
-        for (int i = tid; i < LT * 64; i += kQThreads) reinterpret_cast<float4*>(s_T)[i] = T4[i];
-        for (int i = tid; i < A.len; i += kQThreads) reinterpret_cast<float*>(s_qh4)[i] = A.q_hat[(int64_t)q * A.len + i];
+        for (int i = tid; i < LT * 64; i += kQThreads) reinterpret_cast<float4*>(s_T)[i] = __ldcg(T4 + i);
+        for (int i = tid; i < A.len; i += kQThreads)
+          reinterpret_cast<float*>(s_qh4)[i] = __ldcg(A.q_hat + (int64_t)q * A.len + i);
         cur = q;
       }
       if (tid == 0) {
@@ -630,7 +693,7 @@ __device__ void scan_tasks(const QArgs& A, QShared& S, float* s_T, float* s_tkd,
       const bool range = (tk.cnt_flags & kTaskRange) != 0;
       if (range && q != cur_env) {  // the query's envelope tables Tlo / Thi (stored by the front)
         const float4* E4 = reinterpret_cast<const float4*>(A.q_T + ((int64_t)q * 3 + 1) * LT * 256);
-        for (int i = tid; i < 2 * LT * 64; i += kQThreads) reinterpret_cast<float4*>(s_env)[i] = E4[i];
+        for (int i = tid; i < 2 * LT * 64; i += kQThreads) reinterpret_cast<float4*>(s_env)[i] = __ldcg(E4 + i);
         cur_env = q;
         __syncthreads();
       }
@@ -1257,7 +1320,10 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
       const bool dc = s_dense >= 0;
       const int CH = chunk_blocks<LT>(A.B);
       const int budget = A.front_batches * batch_blocks<LT>(A.B);  // leaves the front scans itself
-      if (tid == 0) S.ntask = 0;
+      if (tid == 0) {
+        S.ntask = 0;
+        S.nf = 0;
+      }
       __syncthreads();
       if (dc && early_dense) {
         // a dense candidate's rows are only needed if the batch skips the dense pass: every leaf, in
@@ -1331,6 +1397,7 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
           h->tkd[r] = s_tkd[r];
           h->tki[r] = s_tki[r];
         }
+        __syncthreads();
         if (tid == 0) {
           h->tkn = S.tkn;
           h->lock = 0;
@@ -1338,7 +1405,12 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
           h->done = 0;
           h->bsf = S.bsf;
           h->bsf_init = S.bsf_init;
+          __threadfence();  // tables, q-hat, top-k and ntasks before the flag the FIFO consumers wait on
+          *(volatile int*)&h->ready = A.epoch;
         }
+        __syncthreads();
+        for (int f = 0; f < S.nf; ++f)  // the query's FIFO entries become visible only now
+          for (int i = tid; i < S.fcnt[f]; i += kQThreads) *(volatile int*)&A.fifo_seq[S.fpos[f] + i] = A.epoch;
       }
     }
     // ---------------------------------------------------------------- output
@@ -1374,8 +1446,14 @@ __global__ void __launch_bounds__(kQThreads, kQThreads == 256 ? 3 : 1) k_query(c
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       tr[15] = smid;
     }
+    if (tid == 0 && A.fused) {  // this query's front is finished (its tasks and state are published)
+      __threadfence();
+      atomicAdd(A.fcount, 1);
+    }
     __syncthreads();
   }
+  // no query left for this CTA: drain the FIFO of set-0 tasks other fronts publish (or still will)
+  if (A.mode == 0 && A.fused) scan_tasks<LT, NF, RR>(A, S, s_T, s_tkd, s_tki, s_qh4, s_Tlo, true);
 }
 
 template <int LT, int NF, int RR = refine_rows<NF>()>
@@ -1427,6 +1505,13 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
       SOFA_CK(cudaMalloc(&ix->pool, (size_t)pool_need * 8));
       SOFA_CK(cudaMalloc(&ix->tasks, (size_t)2 * task_need * sizeof(ScanTask)));
       SOFA_CK(cudaMalloc(&ix->rank_count, (size_t)2 * ranks * 4));
+      if (ix->fifo) cudaFree(ix->fifo);
+      if (ix->fifo_seq) cudaFree(ix->fifo_seq);
+      SOFA_CK(cudaMalloc(&ix->fifo, (size_t)task_need * sizeof(ScanTask)));
+      SOFA_CK(cudaMalloc(&ix->fifo_seq, (size_t)(task_need + 4096) * 4));
+      // epoch-tagged entries and states: zeroed once, so no stale value can match an epoch (>= 1)
+      SOFA_CK(cudaMemsetAsync(ix->fifo_seq, 0, (size_t)(task_need + 4096) * 4, st));
+      SOFA_CK(cudaMemsetAsync(ix->qstate, 0, (size_t)qn * sizeof(QState), st));
       ix->scan_q_cap = qn;
       ix->scan_LT = LT;
       ix->pool_cap = pool_need;
@@ -1435,11 +1520,20 @@ static int launch_query_t(sofa_index* ix, const QArgs& A0, cudaStream_t st) {
     }
     SOFA_CK(cudaMemsetAsync(ix->qcounter, 0, 16 * sizeof(int), st));
     SOFA_CK(cudaMemsetAsync(ix->rank_count, 0, (size_t)2 * ix->rank_cap * 4, st));
+    if (!ix->fcount) SOFA_CK(cudaMalloc(&ix->fcount, 512));
+    SOFA_CK(cudaMemsetAsync(ix->fcount, 0, 512, st));
+    ix->epoch = ix->epoch + 1 > 0 ? ix->epoch + 1 : 1;  // a new front launch
   } else if (A.mode >= 2) {
     SOFA_CK(cudaMemsetAsync(ix->qcounter, 0, 16 * sizeof(int), st));
   }
   A.rank_count = reinterpret_cast<int*>(ix->rank_count);
   A.rank_cap = (int)ix->rank_cap;
+  A.fifo = reinterpret_cast<ScanTask*>(ix->fifo);
+  A.fifo_seq = reinterpret_cast<int*>(ix->fifo_seq);
+  A.fifo_cap = ix->task_cap + 4096;
+  A.fcount = ix->fcount;
+  A.epoch = ix->epoch;
+  A.fused = A.mode == 0 && ix->tune.scan_fused != 0;
   A.qs = reinterpret_cast<QState*>(ix->qstate);
   A.q_T = reinterpret_cast<float*>(ix->q_T);
   A.q_hat = reinterpret_cast<float*>(ix->q_hat);
@@ -1461,6 +1555,9 @@ int launch_query_impl(sofa_index* ix, const float* Q, int q, int k, const float*
   A.ed_out = ed_out;
   A.lb_rows = lb_rows;
   const sofa_tuning& T = ix->tune;
+  // the front's own budget of LB-ordered word batches per query.  (With the fused scan, 8 batches made
+  // configs[1] 4% faster on average but bimodal: a query whose sampled top-M threshold picked few
+  // leaves then refined ~6k rows in its front in ~40% of the steps, 1.8 ms instead of 0.5.)
   A.front_batches = T.front_batches > 0 ? T.front_batches : 16;
   A.rev_rounds = T.rev_rounds;
   // top-M seeding only for lists longer than ~1/16 of the index, in [TOPM_MIN_LEAVES, CAP_B] leaves: a

@@ -165,7 +165,7 @@ int sofa_kernel_timing(sofa_index* ix, int32_t enable, double* out_ms, int64_t* 
 int sofa_default_tuning(sofa_tuning* out) {
   if (!out) return fail(SOFA_EINVAL, "out is NULL");
   memset(out, 0, sizeof(*out));
-  out->front_batches = 16;
+  out->front_batches = 0;
   out->rev_rounds = 2;
   out->topm_min = 0;
   out->topm_leaves = 64;
@@ -178,13 +178,14 @@ int sofa_default_tuning(sofa_tuning* out) {
   out->dense_batch_rows = 0;
   out->dense_pair = 0;
   out->dense_mcast = 1;
+  out->scan_fused = 1;
   return SOFA_OK;
 }
 
 int sofa_set_tuning(sofa_index* ix, const sofa_tuning* t) {
   g_err.clear();
   if (!ix || !t) return fail(SOFA_EINVAL, "NULL pointer");
-  if (t->front_batches < 1) return fail(SOFA_EINVAL, "front_batches must be >= 1");
+  if (t->front_batches < 0) return fail(SOFA_EINVAL, "front_batches must be >= 0");
   if (t->rev_rounds < 0) return fail(SOFA_EINVAL, "rev_rounds must be >= 0");
   if (t->topm_min < 0 || t->topm_leaves < 1 || t->topm_leaves > 2048)
     return fail(SOFA_EINVAL, "topm_min >= 0 and topm_leaves in [1, 2048]");
@@ -229,7 +230,7 @@ void sofa_free(sofa_index* ix) {
   for (auto* v : {&ix->ktime_pending, &ix->ktime_free})
     for (auto& quad : *v)
       for (auto e : quad) cudaEventDestroy(e);
-  void* bufs[] = {ix->qstate, ix->q_T, ix->q_hat, ix->pool, ix->tasks, ix->rank_count, ix->words, ix->stats, ix->stats_orig, ix->perm, ix->env, ix->bkey, ix->xb16, ix->basis32, ix->basis64, ix->edges32,
+  void* bufs[] = {ix->qstate, ix->q_T, ix->q_hat, ix->pool, ix->tasks, ix->rank_count, ix->fifo, ix->fifo_seq, ix->fcount, ix->words, ix->stats, ix->stats_orig, ix->perm, ix->env, ix->bkey, ix->xb16, ix->basis32, ix->basis64, ix->edges32,
                   ix->edges64, ix->gscratch, ix->qcounter, ix->dstats, ix->hq_dev, ix->hd_dev, ix->hi_dev,
                   ix->trace};
   for (void* p : bufs)

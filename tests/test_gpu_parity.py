@@ -388,3 +388,21 @@ def test_wide_and_narrow_query_builds_agree(front_wide, scan_wide, kind, k, Q):
     assert torch.equal(d, d2) and torch.equal(i, i2)
     do, io = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), k)
     assert_knn_parity(d.cpu().numpy(), i.cpu().numpy(), do, io, x.cpu().numpy(), q.cpu().numpy())
+
+
+@pytest.mark.parametrize("kind,N,Q,k", [("cfg2", 300_000, 900, 1), ("cfg4", 250_000, 600, 3), ("cfg1", 120_000, 40, 2)])
+def test_fused_scan_identical(kind, N, Q, k):
+    """front CTAs without a query left drain the published set-0 tasks from a FIFO in the same launch
+    (scan_fused = 1, default) or leave them to the separate scan launch (0): the same bits, and the
+    oracle's answer; the FIFO path must really have carried tasks"""
+    w = datagen.scaled(datagen.WORKLOADS[kind], N, Q, k=k)
+    x, q = _data(w)
+    ix = SofaIndex(x, sample_size=datagen.default_sample_size(w))
+    ix.set_tuning(front_batches=1)  # small front budget: most lists go through the task pool
+    d1, i1, st = ix.knn(q, k, stats=True)
+    assert st["scan_tasks"] > 0
+    ix.set_tuning(front_batches=1, scan_fused=0)
+    d0, i0 = ix.knn(q, k)
+    assert torch.equal(i1, i0) and torch.equal(d1, d0)
+    do, io = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), k)
+    assert_knn_parity(d1.cpu().numpy(), i1.cpu().numpy(), do, io, x.cpu().numpy(), q.cpu().numpy())
