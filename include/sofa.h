@@ -157,6 +157,9 @@ typedef struct {
                               number of query groups the two CTAs of a cluster serve two groups over the
                               same row tiles and share each tile by TMA multicast (one L2 read per tile
                               for both); 0 = one CTA per worker (cooperative launch) */
+  int32_t dense_klist;     /* k > 1: the screen's upper-bound lists (the k smallest UB_g of candidate rows,
+                              which lower a query's threshold): 0 = per CTA in shared memory when they fit
+                              (default), 1 = one list per query in global memory under a lock */
   int32_t scan_fused;      /* front CTAs that find no query left scan the tasks other fronts publish, in the
                               same launch (default 1); 0 = only the separate scan launch scans them */
 } sofa_tuning;

@@ -262,6 +262,7 @@ struct DenseScratch {
   unsigned long long* key1 = nullptr;  // slot: k = 1 best as (d^2 bits << 32 | local row), lock-free min
   int* lock = nullptr;
   float* ubl = nullptr;            // slot x k_cap: k smallest upper bounds of candidate rows (k > 1)
+  float* ubsnap = nullptr;         // slot x screen CTA x (k_cap + 2): each CTA's UB list, seqlock-published (k > 1)
   int* ubn = nullptr;
   int* ub_lock = nullptr;
   int* overflow = nullptr;

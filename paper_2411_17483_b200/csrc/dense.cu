@@ -202,9 +202,18 @@ struct DenseArgs {
   int raw_ld;
   int raw_q;      // debug: number of query slots (instead of *qd_count)
   int diag;       // sofa_tuning.dense_diag (timing diagnostics; 0 in real use)
+  int global_lists;  // k > 1: one UB list per query under a lock instead of per-CTA lists (sofa_tuning.dense_klist)
+  float* ubsnap;     // k > 1 with per-CTA lists: their published copies, slot x cpg_cap x (k + 2) (zeroed per call)
+  int cpg_cap;
   int cluster2;   // single-CTA screen launched as clusters of 2: an even number of query groups shares
                   // every row tile by TMA multicast (one L2 read feeds both CTAs of the cluster)
 };
+
+__device__ __forceinline__ float warp_min_f32(float v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = fminf(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
 
 // shared-memory float minimum (values of either sign), rare path
 __device__ __forceinline__ void smem_fmin(float* p, float v) {
@@ -222,6 +231,8 @@ struct UbLists {
   float* l;
   int* n;
   int* lock;
+  float* snap0;       // nullable: this CTA's published copy of its list for query slot 0 (seqlock: seq, n, values)
+  int64_t snap_slot;  // floats between consecutive slots' copies
 };
 
 // a candidate row's upper bound UB_g lowers the query's threshold: k = 1 directly; k > 1 through
@@ -253,6 +264,16 @@ __device__ void offer_ub(const DenseArgs& A, int slot, int col, float ub, float*
       const int nn = n < A.k ? n + 1 : A.k;
       *(volatile int*)&L.n[col] = nn;
       if (nn == A.k) t = l[A.k - 1];
+      if (L.snap0) {  // publish the list (seqlock, this CTA is its only writer) for the union bound
+        volatile int* sn = reinterpret_cast<volatile int*>(L.snap0 + (int64_t)slot * L.snap_slot);
+        const int s0 = sn[0];
+        sn[0] = s0 + 1;
+        __threadfence();
+        sn[1] = nn;
+        for (int j = 0; j < nn; ++j) reinterpret_cast<volatile float*>(sn)[2 + j] = l[j];
+        __threadfence();
+        sn[0] = s0 + 2;
+      }
     }
     __threadfence_block();
     atomicExch(lk, 0);
@@ -369,7 +390,7 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   const int sbytes = str ? 2 * DA_BYTES + nq * 128 : DA_BYTES; // one ring stage: a K chunk of the unit
   // k > 1: per-CTA UB lists in shared memory if they fit next to a ring of >= 3 stages (else global)
   const int lbytes = A.k > 1 ? (nq * A.k * 4 + nq * 8 + 15) / 16 * 16 : 0;
-  const bool local_lists = A.k > 1 && !A.raw_out && A.smem_dyn - 1024 - bres - D_MISC - lbytes >= 3 * sbytes;
+  const bool local_lists = A.k > 1 && !A.raw_out && !A.global_lists && A.smem_dyn - 1024 - bres - D_MISC - lbytes >= 3 * sbytes;
   int S = (A.smem_dyn - 1024 - bres - D_MISC - (local_lists ? lbytes : 0)) / sbytes;  // as deep as the rest allows
   S = S > D_MAX_STAGES ? D_MAX_STAGES : S;
   unsigned char* sB = dsm;                                     // RES: KC x nqb x 128 B
@@ -377,11 +398,17 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   float* s_d = reinterpret_cast<float*>(sA + (size_t)S * sbytes);  // nq: thr + eps - |q^|^2
   float* s_qn = s_d + 256;                                         // nq: |q^|^2
   float* s_eps = s_qn + 256;                                       // nq: eps
-  UbLists L{nullptr, nullptr, nullptr};
+  UbLists L{nullptr, nullptr, nullptr, nullptr, 0};
+  // the group's list writers (CTAs, or both CTAs of each pair) and this CTA's index among them
+  const int nwr = PAIR ? 2 * cpg : cpg, me = PAIR ? 2 * twin + (int)rank : twin;
   if (local_lists) {
     L.l = s_eps + 256;           // nq x k
     L.n = reinterpret_cast<int*>(L.l + nq * A.k);
     L.lock = L.n + nq;
+    if (A.ubsnap && !idle && nwr <= A.cpg_cap) {
+      L.snap0 = A.ubsnap + (int64_t)me * (A.k + 2);
+      L.snap_slot = (int64_t)A.cpg_cap * (A.k + 2);
+    }
   }
   uint64_t* full = bars;                   // [S]
   uint64_t* empty = bars + D_MAX_STAGES;   // [S]
@@ -592,6 +619,50 @@ __global__ void __launch_bounds__(D_THREADS, 1)
         for (int c = lane; c < nqv; c += 32) {
           const float nd = *(volatile float*)&A.thr[q0 + c] + s_eps[c] - s_qn[c];
           if (nd < s_d[c]) smem_fmin(s_d + c, nd);
+        }
+        if (L.snap0) {
+          // k > 1: the union bound.  Every writer's list holds UB_g of distinct rows of its own tiles, so
+          // the k-th smallest of the values read from ANY of the lists (here each writer's two smallest,
+          // torn or in-progress copies skipped) bounds the query's k-th best — far tighter than one CTA's
+          // own k-th.  This CTA computes it for its share of the group's columns.
+          for (int c = me; c < nqv; c += nwr) {
+            float vals[10];
+#pragma unroll
+            for (int j = 0; j < 10; ++j) vals[j] = INFINITY;
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+              const int t = lane + 32 * j;
+              if (t >= nwr) break;
+              const volatile int* sn =
+                  reinterpret_cast<const volatile int*>(A.ubsnap + ((int64_t)(q0 + c) * A.cpg_cap + t) * (A.k + 2));
+              const int s1 = sn[0];
+              if (s1 & 1) continue;
+              const int n = sn[1];
+              const float v0 = n > 0 ? reinterpret_cast<const volatile float*>(sn)[2] : INFINITY;
+              const float v1 = n > 1 ? reinterpret_cast<const volatile float*>(sn)[3] : INFINITY;
+              if (sn[0] != s1) continue;
+              vals[2 * j] = v0;
+              vals[2 * j + 1] = v1;
+            }
+            float v = -INFINITY;
+            int cnt = 0;
+            while (cnt < A.k) {  // the k-th smallest with multiplicity
+              float m = INFINITY;
+#pragma unroll
+              for (int j = 0; j < 10; ++j) m = vals[j] > v ? fminf(m, vals[j]) : m;
+              m = warp_min_f32(m);
+              if (!(m < INFINITY)) break;
+              int e = 0;
+#pragma unroll
+              for (int j = 0; j < 10; ++j) e += vals[j] == m;
+              cnt += __reduce_add_sync(FULL, e);
+              v = m;
+            }
+            if (cnt >= A.k && lane == 0) {
+              atomicMin(reinterpret_cast<unsigned int*>(&A.thr[q0 + c]), __float_as_uint(v));
+              smem_fmin(s_d + c, v + s_eps[c] - s_qn[c]);
+            }
+          }
         }
         __nanosleep(1000);
       }
@@ -991,12 +1062,15 @@ static void fill_screen_args(sofa_index* ix, int k, DenseArgs& A) {
   dense_geometry(ix->len, ix->tune.dense_pair != 0, A.nq_max, A.streamed);
   A.pair = !A.streamed && ix->tune.dense_pair != 0;
   A.cluster2 = !A.pair && ix->tune.dense_mcast != 0;
+  A.global_lists = ix->tune.dense_klist == 1;
   A.smem_dyn = D_SMEM_MAX;
   A.stats_orig = ix->stats_orig;
   A.qd_count = D.counters;
   A.qparams = D.qparams;
   A.thr = D.thr;
   A.ubl = D.ubl;
+  A.ubsnap = k > 1 ? D.ubsnap : nullptr;
+  A.cpg_cap = ix->sms;
   A.ubn = D.ubn;
   A.ub_lock = D.ub_lock;
   A.cand = D.cand;
@@ -1021,6 +1095,7 @@ int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stat
   }
   DenseArgs A{};
   fill_screen_args(ix, k, A);
+  if (A.ubsnap) SOFA_CK(cudaMemsetAsync(A.ubsnap, 0, (size_t)q * ix->sms * (k + 2) * 4, st));
   int sgrid = ix->sms & ~1;
   if ((rc = launch_screen(ix, *reinterpret_cast<const CUtensorMap*>(D.tmap_x),
                           *reinterpret_cast<const CUtensorMap*>(D.tmap_q), A, D_SMEM_MAX,
@@ -1147,6 +1222,7 @@ int ensure_dense_scratch(sofa_index* ix, int q, int k) {
   SOFA_CK(cudaMalloc(&D.key1, (size_t)q * 8));
   SOFA_CK(cudaMalloc(&D.lock, (size_t)q * 4));
   SOFA_CK(cudaMalloc(&D.ubl, (size_t)q * k * 4));
+  if (k > 1) SOFA_CK(cudaMalloc(&D.ubsnap, (size_t)q * ix->sms * (k + 2) * 4));
   SOFA_CK(cudaMalloc(&D.ubn, (size_t)q * 4));
   SOFA_CK(cudaMalloc(&D.ub_lock, (size_t)q * 4));
   SOFA_CK(cudaMalloc(&D.overflow, (size_t)q * 4));
@@ -1158,7 +1234,7 @@ int ensure_dense_scratch(sofa_index* ix, int q, int k) {
 
 void free_dense_scratch(sofa_index* ix) {
   DenseScratch& D = ix->dense;
-  void* ps[] = {D.qhat, D.qb16, D.qparams, D.qidx, D.binit, D.bsf, D.thr, D.tkd, D.tki, D.tkn, D.key1, D.lock, D.ubl,
+  void* ps[] = {D.qhat, D.qb16, D.qparams, D.qidx, D.binit, D.bsf, D.thr, D.tkd, D.tki, D.tkn, D.key1, D.lock, D.ubl, D.ubsnap,
                 D.ubn, D.ub_lock, D.overflow, D.ovf_list, D.cand, D.counters};
   for (void* p : ps)
     if (p) cudaFree(p);

@@ -58,7 +58,8 @@ class sofa_tuning(C.Structure):
     _fields_ = [(f, C.c_int32) for f in ("front_batches", "rev_rounds", "topm_min", "topm_leaves",
                                          "refine_rows_front", "refine_rows_scan", "front_wide", "scan_wide")] + \
         [("dense_cand_cap", C.c_int64), ("dense_batch_rows", C.c_int64), ("dense_pair", C.c_int32),
-         ("dense_diag", C.c_int32), ("dense_mcast", C.c_int32), ("scan_fused", C.c_int32)]
+         ("dense_diag", C.c_int32), ("dense_mcast", C.c_int32), ("dense_klist", C.c_int32),
+         ("scan_fused", C.c_int32)]
 
 
 class sofa_knn_stats(C.Structure):
