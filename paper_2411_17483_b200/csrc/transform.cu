@@ -20,10 +20,14 @@
 //     in shared memory; float32 rounding moves a value by ~1e-7 relative, inside reading 24's
 //     1e-5 edge exemption), the a4 key bits of the lane's symbols OR-reduced over the group;
 //   * optionally the z-normalised row as bfloat16 (original row order) for the dense screen (f1).
-// Work per n = 256 row: 64 warp-FFMA (folded) + ~120 other instructions, i.e. ~45 SM cycles, below
-// the ~43-cycle HBM budget of one 1 KB row per SM only with good overlap — the kernel is designed to
-// be HBM-bound, not measured to be here (see profiles/).  The accuracy budget (symbols bit-exact
-// outside 1e-5 of an edge, SURVEY 8(c) reading 24) rules out 1xTF32 tensor cores.
+// Measured (B200, configs[2], 10M x 256, tools/transform_probe.py): 3.5 TB/s of algorithmic bytes
+// (10.24 GB read + 5.39 GB written in ~4.5 ms), 0.53 of the measured copy bandwidth: instruction- and
+// latency-bound, not HBM-bound.  Round 2: the Re/Im operand choice is a warp-uniform branch per basis
+// row (a register swap at the runtime Re/Im boundary made the compiler carry both assignments: ~500
+// moves per row group), 80 registers for 3 CTAs per SM, and (G <= 8) the next row group is bulk-copied
+// into a per-warp shared-memory buffer while the current one is transformed: 2.93 -> 3.50 TB/s.
+// The accuracy budget (symbols bit-exact outside 1e-5 of an edge, SURVEY 8(c) reading 24) rules out
+// 1xTF32 tensor cores.
 #include <cub/cub.cuh>
 
 #include <cuda_bf16.h>
@@ -55,6 +59,32 @@ __device__ __forceinline__ void reduce_scatter_g(float* v, int lane) {
   }
 }
 
+// one bulk copy (TMA, 1D) of a warp's next rows into its shared-memory buffer, completion counted on
+// the warp's mbarrier: the loads of row group i + 1 are in flight while group i is transformed
+__device__ __forceinline__ void tr_mbar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(b)) : "memory");
+}
+__device__ __forceinline__ void tr_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void tr_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(b), "r"(parity)
+        : "memory");
+}
+constexpr int kTrBuf = 4096;  // bytes per warp: RPW rows of len <= 32 G floats
+
 constexpr int kEdgeLd = 257;  // shared-memory row stride of the edge table (floats)
 
 struct TransformArgs {
@@ -76,12 +106,15 @@ struct TransformArgs {
 
 // 2 CTAs (16 warps, up to 128 registers) when the fold or wide words need the registers, else 3
 template <int G, int LT, bool FOLD>
-__global__ void __launch_bounds__(kThreads, (FOLD || LT > 16) ? 2 : 3) k_transform(const __grid_constant__ TransformArgs A) {
+__global__ void __launch_bounds__(kThreads, LT > 16 ? 2 : 3) k_transform(const __grid_constant__ TransformArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int RPW = 32 / G;                 // rows per warp
   constexpr int NS = FOLD ? 4 : 8;            // basis slots per lane
   constexpr int VPL = LT >= G ? LT / G : 1;   // reduced values per lane
   constexpr int OWN = LT >= G ? 1 : G / LT;   // lanes sharing one value when LT < G
+  // bulk-copy prefetch of the next row group (G <= 8: the basis loads broadcast over the warp's rows);
+  // at G >= 16 the basis loads already fill shared-memory bandwidth and the rows load directly
+  constexpr bool PREF = G <= 8;
   const int len = A.len, nf4 = len >> 2, l = A.l;
   float4* s_basis = reinterpret_cast<float4*>(smem);                           // LT x NS x G
   // LT x kEdgeLd (model order): rows padded to 257 floats so that the lanes of a warp, each searching
@@ -89,6 +122,9 @@ __global__ void __launch_bounds__(kThreads, (FOLD || LT > 16) ? 2 : 3) k_transfo
   float* s_edges = reinterpret_cast<float*>(smem + (size_t)LT * NS * G * 16);
   uint8_t* s_w = reinterpret_cast<uint8_t*>(s_edges + LT * kEdgeLd);          // 8 warps x RPW x LT
   int* s_ord = reinterpret_cast<int*>(s_w + 8 * RPW * LT);                      // LT
+  // 8 warps x kTrBuf (16-byte aligned) row buffers, then 8 mbarriers
+  unsigned char* s_xb = smem + (((size_t)LT * NS * G * 16 + (size_t)LT * kEdgeLd * 4 + 8 * RPW * LT + LT * 4 + 15) & ~(size_t)15);
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_xb + 8 * kTrBuf);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane & (G - 1), rw = lane / G;  // lane in group, row of the warp
   for (int i = tid; i < LT * NS * G; i += kThreads) s_basis[i] = reinterpret_cast<const float4*>(A.basis)[i];
@@ -102,19 +138,55 @@ __global__ void __launch_bounds__(kThreads, (FOLD || LT > 16) ? 2 : 3) k_transfo
   const int P = l < 16 ? l : 16;  // key positions
   const int sh8 = 8 - A.a_bits;
 
-  for (int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * RPW; r0 < A.N; r0 += (int64_t)gridDim.x * 8 * RPW) {
+  const int64_t rstride = (int64_t)gridDim.x * 8 * RPW;
+  unsigned char* my_xb = s_xb + warp * kTrBuf;
+  uint64_t* my_bar = s_bar + warp;
+  // the warp's RPW rows are contiguous in the series (row stride = len floats): one bulk copy of
+  // min(RPW, N - r0) rows (len % 4 == 0: 16-byte aligned, a multiple of 16 bytes)
+  auto issue = [&](int64_t r) {
+    if (PREF && lane == 0 && r < A.N) {
+      const int64_t nr = A.N - r < RPW ? A.N - r : RPW;
+      tr_bulk_load(my_xb, A.X + r * len, (uint32_t)(nr * len * 4), my_bar);
+    }
+  };
+  if (PREF && lane == 0) {
+    tr_mbar_init(my_bar);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t xphase = 0;
+  issue(((int64_t)blockIdx.x * 8 + warp) * RPW);
+  for (int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * RPW; r0 < A.N; r0 += rstride) {
     const int64_t row = r0 + rw;
     const bool live = row < A.N;
-    const float4* xr = reinterpret_cast<const float4*>(A.X + row * len);
     float4 x[8];
+    if constexpr (PREF) {
+      tr_wait(my_bar, xphase);
+      xphase ^= 1u;
+      const float4* xr = reinterpret_cast<const float4*>(my_xb) + rw * nf4;
 #pragma unroll
-    for (int f = 0; f < 8; ++f) {
-      const int fi = g + G * f;
-      x[f] = (live && fi < nf4) ? ld_stream(xr + fi) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int f = 0; f < 8; ++f) {
+        const int fi = g + G * f;
+        x[f] = (live && (FOLD || fi < nf4)) ? xr[fi] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    } else {
+      const float4* xr = reinterpret_cast<const float4*>(A.X + row * len);
+#pragma unroll
+      for (int f = 0; f < 8; ++f) {
+        const int fi = g + G * f;
+        x[f] = (live && (FOLD || fi < nf4)) ? ld_stream(xr + fi) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
     float muf;
     double mu64, inv64;
-    row_stats_g<G>(x, nf4, g, len, muf, mu64, inv64);
+    row_stats_g<G, FOLD>(x, nf4, g, len, muf, mu64, inv64);  // FOLD implies n = 32 G
+    // every lane has consumed its buffer values (the statistics use all of them): the buffer may be
+    // refilled with the next row group while this one is transformed
+    if constexpr (PREF) {
+      __syncwarp();
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(r0 + rstride);
+    }
 #pragma unroll
     for (int f = 0; f < 8; ++f) {
       x[f].x = __fsub_rn(x[f].x, muf);
@@ -127,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, (FOLD || LT > 16) ? 2 : 3) k_transfo
 #pragma unroll
       for (int f = 0; f < 8; ++f) {
         const int fi = g + G * f;
-        if (fi < nf4) {
+        if (FOLD || fi < nf4) {
           __nv_bfloat162 lo = __floats2bfloat162_rn(x[f].x * invf, x[f].y * invf);
           __nv_bfloat162 hi = __floats2bfloat162_rn(x[f].z * invf, x[f].w * invf);
           uint2 pk;
@@ -159,29 +231,34 @@ __global__ void __launch_bounds__(kThreads, (FOLD || LT > 16) ? 2 : 3) k_transfo
         x[7 - f] = make_float4(__fsub_rn(a.x, p0), __fsub_rn(a.y, p1), __fsub_rn(a.z, p2), __fsub_rn(a.w, p3));
       }
       if (g == 0) x[0].x = __fadd_rn(x0, nyq);  // u_0 = x_0 + x_{n/2}: exact for Re rows with even k
-      // processing rows [Re | Im]: u (x[0..3]) for the Re rows, then the registers are swapped once so
-      // that x[0..3] hold v for the Im rows (one uniform check per row instead of a select per value)
+      // processing rows [Re | Im]: u (x[0..3]) for the Re rows, v (x[7..4]) for the Im rows.  One
+      // warp-uniform branch per row picks the operand registers (a register swap at the runtime
+      // boundary j == nre made the compiler carry both assignments through the unrolled loop: ~500
+      // register moves per row group)
       const float4* bs = s_basis + g;
 #pragma unroll
       for (int j = 0; j < LT; ++j) {
-        if (j == nre) {
+        float s = acc[j];
+        if (j < nre) {
 #pragma unroll
           for (int f = 0; f < 4; ++f) {
-            const float4 t = x[f];
-            x[f] = x[7 - f];
-            x[7 - f] = t;
+            const float4 b = bs[(j * 4 + f) * G];
+            s = fmaf(x[f].x, b.x, s);
+            s = fmaf(x[f].y, b.y, s);
+            s = fmaf(x[f].z, b.z, s);
+            s = fmaf(x[f].w, b.w, s);
+          }
+        } else {
+#pragma unroll
+          for (int f = 0; f < 4; ++f) {
+            const float4 b = bs[(j * 4 + f) * G];
+            s = fmaf(x[7 - f].x, b.x, s);
+            s = fmaf(x[7 - f].y, b.y, s);
+            s = fmaf(x[7 - f].z, b.z, s);
+            s = fmaf(x[7 - f].w, b.w, s);
           }
         }
-#pragma unroll
-        for (int f = 0; f < 4; ++f) {
-          const float4 b = bs[(j * 4 + f) * G];
-          float s = acc[j];
-          s = fmaf(x[f].x, b.x, s);
-          s = fmaf(x[f].y, b.y, s);
-          s = fmaf(x[f].z, b.z, s);
-          s = fmaf(x[f].w, b.w, s);
-          acc[j] = s;
-        }
+        acc[j] = s;
       }
       nyq_row = __shfl_sync(FULL, nyq, lane & ~(G - 1));
     } else {
@@ -330,7 +407,8 @@ static int launch_transform_t(const TransformArgs& A0, const DevModel& dm, const
   A.n_re_odd = no;
   constexpr int RPW = 32 / G, NS = FOLD ? 4 : 8;
   auto kern = k_transform<G, LT, FOLD>;
-  const size_t smem = (size_t)LT * NS * G * 16 + (size_t)LT * kEdgeLd * 4 + 8 * RPW * LT + LT * 4;
+  const size_t smem = (((size_t)LT * NS * G * 16 + (size_t)LT * kEdgeLd * 4 + 8 * RPW * LT + LT * 4 + 15) & ~(size_t)15) +
+                      (G <= 8 ? 8 * kTrBuf + 8 * 8 : 0);  // PREF: row buffers + mbarriers
   SOFA_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
