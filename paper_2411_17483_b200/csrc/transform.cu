@@ -236,29 +236,72 @@ __global__ void __launch_bounds__(kThreads, LT > 16 ? 2 : 3) k_transform(const _
       // boundary j == nre made the compiler carry both assignments through the unrolled loop: ~500
       // register moves per row group)
       const float4* bs = s_basis + g;
+      // blocks of JB basis rows: a block entirely on one side of the Re/Im boundary runs its rows
+      // slot by slot (JB independent FFMA chains, JB x 4 basis loads the compiler can issue ahead:
+      // the per-row form stalled ~20% of the samples on each row's own four loads); the one block
+      // that straddles the boundary falls back to a branch per row.  Per row the FFMA order is
+      // unchanged (slots 0..3, components x..w): the same float32 bits.
+      constexpr int JB = LT > 16 ? 4 : 1;  // blocks only where 128 registers are available (2 CTAs/SM)
+      auto rows_re = [&](int j0) {
 #pragma unroll
-      for (int j = 0; j < LT; ++j) {
-        float s = acc[j];
-        if (j < nre) {
+        for (int f = 0; f < 4; ++f)
 #pragma unroll
-          for (int f = 0; f < 4; ++f) {
-            const float4 b = bs[(j * 4 + f) * G];
+          for (int jj = 0; jj < JB; ++jj) {
+            const float4 b = bs[((j0 + jj) * 4 + f) * G];
+            float s = acc[j0 + jj];
             s = fmaf(x[f].x, b.x, s);
             s = fmaf(x[f].y, b.y, s);
             s = fmaf(x[f].z, b.z, s);
             s = fmaf(x[f].w, b.w, s);
+            acc[j0 + jj] = s;
           }
-        } else {
+      };
+      auto rows_im = [&](int j0) {
 #pragma unroll
-          for (int f = 0; f < 4; ++f) {
-            const float4 b = bs[(j * 4 + f) * G];
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+          for (int jj = 0; jj < JB; ++jj) {
+            const float4 b = bs[((j0 + jj) * 4 + f) * G];
+            float s = acc[j0 + jj];
             s = fmaf(x[7 - f].x, b.x, s);
             s = fmaf(x[7 - f].y, b.y, s);
             s = fmaf(x[7 - f].z, b.z, s);
             s = fmaf(x[7 - f].w, b.w, s);
+            acc[j0 + jj] = s;
+          }
+      };
+#pragma unroll
+      for (int j0 = 0; j0 < LT; j0 += JB) {
+        if (j0 + JB <= nre) {
+          rows_re(j0);
+        } else if (j0 >= nre) {
+          rows_im(j0);
+        } else {
+#pragma unroll
+          for (int j = j0; j < j0 + JB; ++j) {
+            float s = acc[j];
+            if (j < nre) {
+#pragma unroll
+              for (int f = 0; f < 4; ++f) {
+                const float4 b = bs[(j * 4 + f) * G];
+                s = fmaf(x[f].x, b.x, s);
+                s = fmaf(x[f].y, b.y, s);
+                s = fmaf(x[f].z, b.z, s);
+                s = fmaf(x[f].w, b.w, s);
+              }
+            } else {
+#pragma unroll
+              for (int f = 0; f < 4; ++f) {
+                const float4 b = bs[(j * 4 + f) * G];
+                s = fmaf(x[7 - f].x, b.x, s);
+                s = fmaf(x[7 - f].y, b.y, s);
+                s = fmaf(x[7 - f].z, b.z, s);
+                s = fmaf(x[7 - f].w, b.w, s);
+              }
+            }
+            acc[j] = s;
           }
         }
-        acc[j] = s;
       }
       nyq_row = __shfl_sync(FULL, nyq, lane & ~(G - 1));
     } else {
@@ -300,10 +343,17 @@ __global__ void __launch_bounds__(kThreads, LT > 16 ? 2 : 3) k_transform(const _
           my_w[rw * LT + j] = (uint8_t)pos;
           if (j < P) {  // a4 key bits of this position: 2-bit digits, MSB first, round-robin
             const uint32_t s8 = ((uint32_t)pos << sh8) & 0xffu;
+            if (P == 16) {
+              // 16 key positions (warp-uniform): round 0 fills the high word, round 1 the low word,
+              // rounds 2 and 3 fall past bit 0 - two 32-bit shifts instead of four guarded 64-bit ones
+              const int sh = 30 - 2 * j;
+              key |= ((unsigned long long)(((s8 >> 6) & 3u) << sh) << 32) | (unsigned long long)(((s8 >> 4) & 3u) << sh);
+            } else {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              const int o = r * 2 * P + 2 * j;
-              if (o < 64) key |= (unsigned long long)((s8 >> (6 - 2 * r)) & 3u) << (62 - o);
+              for (int r = 0; r < 4; ++r) {
+                const int o = r * 2 * P + 2 * j;
+                if (o < 64) key |= (unsigned long long)((s8 >> (6 - 2 * r)) & 3u) << (62 - o);
+              }
             }
           }
         }
@@ -316,7 +366,10 @@ __global__ void __launch_bounds__(kThreads, LT > 16 ? 2 : 3) k_transform(const _
       if (A.stats) A.stats[row] = make_float2(muf, (float)inv64);
       if (A.keys) A.keys[row] = key;
     }
-    if (A.words) {
+    if (LT == 16 && A.words) {  // WS == 16: one 16-byte word per row, lane s writes row s
+      if (lane < RPW && r0 + lane < A.N)
+        *reinterpret_cast<uint4*>(A.words + (r0 + lane) * 16) = *reinterpret_cast<const uint4*>(my_w + lane * LT);
+    } else if (A.words) {
       const int parts = A.WS >> 4;
       for (int c = lane; c < RPW * parts; c += 32) {
         const int s = c / parts, p = c % parts;
