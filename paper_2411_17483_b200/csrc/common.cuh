@@ -92,15 +92,15 @@ __host__ __device__ constexpr int row_group(int nf4) {
 // sums its float4s in float32, the G partials are combined in float64 by an xor butterfly (every
 // lane of the group ends with the same value).  Returns mu (float32 and float64) and inv_sigma
 // (float64; 0 for a constant row).
-// FULL (compile time): the caller knows nf4 == 8 G (every lane's 8 float4 are in the row): the same
+// ALLSLOTS (compile time; it was once named FULL and shadowed the shuffle mask): the caller knows nf4 == 8 G (every lane's 8 float4 are in the row): the same
 // arithmetic without the per-slot guards.
-template <int G, bool FULL = false>
+template <int G, bool ALLSLOTS = false>
 __device__ __forceinline__ void row_stats_g(const float4 (&x)[8], int nf4, int g, int len, float& muf, double& mu64,
                                             double& inv64) {
   float p = 0.f;
 #pragma unroll
   for (int f = 0; f < 8; ++f)
-    if (FULL || g + G * f < nf4) p = __fadd_rn(p, __fadd_rn(__fadd_rn(x[f].x, x[f].y), __fadd_rn(x[f].z, x[f].w)));
+    if (ALLSLOTS || g + G * f < nf4) p = __fadd_rn(p, __fadd_rn(__fadd_rn(x[f].x, x[f].y), __fadd_rn(x[f].z, x[f].w)));
   double sp = (double)p;
 #pragma unroll
   for (int m = G / 2; m >= 1; m >>= 1) sp += __shfl_xor_sync(FULL, sp, m);
@@ -109,7 +109,7 @@ __device__ __forceinline__ void row_stats_g(const float4 (&x)[8], int nf4, int g
   float s = 0.f;
 #pragma unroll
   for (int f = 0; f < 8; ++f)
-    if (FULL || g + G * f < nf4) {
+    if (ALLSLOTS || g + G * f < nf4) {
       const float a = __fsub_rn(x[f].x, muf), b = __fsub_rn(x[f].y, muf);
       const float c = __fsub_rn(x[f].z, muf), d = __fsub_rn(x[f].w, muf);
       s = __fadd_rn(s, __fadd_rn(__fmaf_rn(a, a, __fmul_rn(b, b)), __fmaf_rn(c, c, __fmul_rn(d, d))));

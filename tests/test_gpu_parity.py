@@ -406,3 +406,19 @@ def test_fused_scan_identical(kind, N, Q, k):
     assert torch.equal(i1, i0) and torch.equal(d1, d0)
     do, io = O.knn_bruteforce(x.cpu().numpy(), q.cpu().numpy(), k)
     assert_knn_parity(d1.cpu().numpy(), i1.cpu().numpy(), do, io, x.cpu().numpy(), q.cpu().numpy())
+
+
+@pytest.mark.parametrize("kind", ["cfg1", "cfg3"])
+def test_stored_row_as_query_has_distance_zero(kind):
+    """a1: the transform's (mu, 1/sigma) of a row and the query prep's of the same values come from one
+    function with one arithmetic order (common.cuh row_stats_g), so they are the same float32 bits and
+    the exact refine of a row against itself is 0.0 (rows of a ragged last warp group included)"""
+    w = datagen.scaled(datagen.WORKLOADS[kind], 25_000 + 2, 4)
+    x = datagen.generate_rows(w, 0, w.n_series, device="cuda")
+    ix = SofaIndex(x, l=16, sample_size=3000)
+    rows = torch.tensor([0, 1, 2, 3, 5, 4097, 12_345, w.n_series - 2, w.n_series - 1], device="cuda")
+    d, i = ix.knn(x[rows].contiguous(), 1)
+    torch.cuda.synchronize()
+    assert torch.all(d[:, 0] == 0.0), d[:, 0]
+    assert torch.equal(x[i[:, 0]], x[rows])  # the row itself, or an exact duplicate of it
+    ix.close()
