@@ -20,12 +20,17 @@
 //     in shared memory; float32 rounding moves a value by ~1e-7 relative, inside reading 24's
 //     1e-5 edge exemption), the a4 key bits of the lane's symbols OR-reduced over the group;
 //   * optionally the z-normalised row as bfloat16 (original row order) for the dense screen (f1).
-// Measured (B200, configs[2], 10M x 256, tools/transform_probe.py): 3.5 TB/s of algorithmic bytes
-// (10.24 GB read + 5.39 GB written in ~4.5 ms), 0.53 of the measured copy bandwidth: instruction- and
-// latency-bound, not HBM-bound.  Round 2: the Re/Im operand choice is a warp-uniform branch per basis
-// row (a register swap at the runtime Re/Im boundary made the compiler carry both assignments: ~500
-// moves per row group), 80 registers for 3 CTAs per SM, and (G <= 8) the next row group is bulk-copied
-// into a per-warp shared-memory buffer while the current one is transformed: 2.93 -> 3.50 TB/s.
+// Measured (B200, configs[2], 10M x 256, tools/transform_probe.py): 3.65 TB/s of algorithmic bytes
+// (10.24 GB read + 5.39 GB written in ~4.3 ms), 0.56 of the measured copy bandwidth.  The bound is the
+// shared-memory LSU pipe (ncu: l1tex__data_pipe_lsu_wavefronts 92% of peak, DRAM 45%, issue 59%): per
+// 4-row warp iteration ~410 wavefronts - 256 for the basis (one wavefront feeds one FFMA warp
+// instruction whatever the load width; the warp's four row groups read the same bytes), 32 for the
+// row buffer, ~57 for the edge searches, ~60 shuffles (DESIGN 12).  Round 2: the Re/Im operand choice
+// is a warp-uniform branch per basis row (a register swap at the runtime Re/Im boundary made the
+// compiler carry both assignments: ~500 moves per row group), 80 registers for 3 CTAs per SM, (G <= 8)
+// the next row group is bulk-copied into a per-warp shared-memory buffer while the current one is
+// transformed, 16-position key bits as two 32-bit shifts and one 16-byte word store per row:
+// 2.93 -> 3.65 TB/s.
 // The accuracy budget (symbols bit-exact outside 1e-5 of an edge, SURVEY 8(c) reading 24) rules out
 // 1xTF32 tensor cores.
 #include <cub/cub.cuh>

@@ -11,16 +11,16 @@ O=gpurun_out/ev
 mkdir -p $O
 NCU="ncu --clock-control none"
 
-# 1. bench lines (no profiler)
+# 1. DRAM traffic per kernel group of this build (bench.py's roofline.traffic)
+for c in cfg4 cfg2 cfg3 cfg1 cfg5; do
+  python tools/traffic.py $c > $O/traffic_$c.log 2>&1 && cp profiles/traffic_$c.json $O/
+done
+
+# 2. bench lines (no profiler; they pick up this build's traffic files)
 for c in cfg4 cfg2 cfg3 cfg1 cfg5; do
   python bench.py --config $c > $O/${R}_bench_$c.json 2> $O/bench_$c.err || echo "bench $c failed" >> $O/errors.log
 done
 python bench.py --impl reference --steps 3 --warmup 1 > $O/${R}_bench_reference_cfg4.json 2> $O/bench_ref.err
-
-# 2. DRAM traffic per kernel group of this build (bench.py's roofline.traffic)
-for c in cfg4 cfg2 cfg3; do
-  python tools/traffic.py $c > $O/traffic_$c.log 2>&1 && cp profiles/traffic_$c.json $O/
-done
 
 # 3. launch list of the default bench command (shares, not absolutes)
 $NCU --metrics gpu__time_duration.sum -k 'regex:k_|Radix' --csv --log-file $O/${R}_ncu_launches_cfg4.csv \
