@@ -445,8 +445,12 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         torch.set_num_threads(cores())
-        rows = min(w.n_series, 1_000_000 if w.length <= 256 else 250_000)
-        nq = 4
+        # ~10 s of host work on 16 cores: the oracle's cost is per row (float64 z-normalisation + GEMM),
+        # so the sample is sized in rows; 3M x 256 needs ~20 GB of host memory in float64 copies
+        import psutil
+        big = psutil.virtual_memory().available > 96e9
+        rows = min(w.n_series, (3_000_000 if big else 1_000_000) * 256 // max(256, w.length))
+        nq = 16
         xs = x[:rows].cpu().numpy()
         qs = q[:nq].cpu().numpy()
         v, dt, desc = oracle_sample(w, rows, nq, xs, qs)
