@@ -88,7 +88,7 @@ typedef struct {
                               passes the bound of its own-key seed, else — once the batch's dense
                               pass is certain — after top-M seeding if >= this many permille pass
                               the tightened bound (and the estimate is >= 4096 rows either way).  The batch runs the tensor-core pass only if
-                              the flagged queries' estimated refines add up to one pass over the
+                              the flagged queries' estimated refines add up to a fifth of a pass over the
                               rows (sofa_tuning.dense_batch_rows); else the scan pool finishes them
                               sparsely.  0 => 5 (0.5%), < 0 => never, >= 1000 => every query
                               (testing).  Results are identical either way; only speed changes. */
@@ -143,8 +143,9 @@ typedef struct {
   int64_t dense_cand_cap;  /* dense-path candidate buffer entries (0 => 16M); a query whose candidates
                               overflow it is rescanned brute force (testing) */
   int64_t dense_batch_rows; /* the batch runs the dense pass iff its flagged queries' estimated sparse
-                              refines add up to at least this many rows (0 => n, one pass over the
-                              rows); a batch below it scans its flagged queries sparsely */
+                              refines add up to at least this many rows (0 => n / 5: the measured
+                              break-even of one bf16 pass over the rows against random-row refines);
+                              a batch below it scans its flagged queries sparsely */
   int32_t dense_pair;      /* dense screen on CTA pairs (tcgen05 cta_group::2, M = 256 rows per MMA, each
                               SM holding half of the query operand) instead of single CTAs (M = 128),
                               for rows of n <= 512 (default 0: measured equal on configs[3] and slower

@@ -350,12 +350,13 @@ int isax_model(int len, int l, int a, sofa_model* out);
 int launch_query(sofa_index* ix, const float* Q, int q, int k, const float* bsf_init, float* od, int64_t* oi,
                  cudaStream_t st, bool scan = false, int64_t lb_m = 0, float* lb_out = nullptr,
                  float* ed_out = nullptr, int64_t* lb_rows = nullptr, float* seed_out = nullptr);
-// batch-level dense decision (f1): run the tensor-core pass iff the flagged queries' estimated sparse
-// refines add up to at least one full pass over the shard's rows
-// the batch decision: the dense pass runs iff the flagged queries' estimated sparse refines add up to at
-// least this many rows (default: one pass over the rows)
+// batch-level dense decision (f1): the tensor-core pass runs iff the flagged queries' estimated sparse
+// refines add up to at least this many rows.  Default n / 5: one dense pass streams 2 len bytes per row
+// at ~6 TB/s, a sparse refine reads 4 len bytes of a random row at ~2.6 TB/s (configs[3], measured), so
+// the pass pays for itself from ~0.22 n refines on (tools/latency_probe.py cfg4: batches of 8 with two
+// or three unprunable queries 23.5 ms at n, 8.9 ms at n / 4 and below; one such query 10.4 -> 8.7 ms)
 inline int64_t dense_batch_rows(const sofa_index* ix) {
-  return ix->tune.dense_batch_rows > 0 ? ix->tune.dense_batch_rows : (ix->n > 0 ? ix->n : 1);
+  return ix->tune.dense_batch_rows > 0 ? ix->tune.dense_batch_rows : (ix->n >= 5 ? ix->n / 5 : 1);
 }
 int launch_dense(sofa_index* ix, int q, int k, float* od, int64_t* oi, bool stats, cudaStream_t st,
                  cudaEvent_t after_screen = nullptr);
